@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py -- Gpoints/s of the acoustic_iso_cd propagator on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--grid 240] [--mode fast|strict] [--radius 4]
+
+A "step" is one time step of the propagator over the whole grid (the
+reference's eng.step(), driver.cpp:104-106).  Workload at N=1: BASELINE.json
+configs[1] -- 240^3 grid, 8th order (r=4), CPML nd=27, taper, Ricker source at
+the centre, 240^2 surface receivers at k=27, default two-layer model
+(synthetic, vp 1500/4500).  Metric: Gpoints/s = n^3 * K / (device time of K
+steps), the reference's points_per_s (bench.cpp:184-186).
+
+Timed region (value): K steps of the device-resident loop (mm_cd_run: source
+injection from a device wavelet, per-step receiver recording and finiteness
+check) bracketed by barrier + synchronize, timed with CUDA events on the
+engine's stream, max over ranks.  The working set (3 pressure fields + c +
+CPML memory, ~290 MB at 240^3) exceeds the 126 MB L2, so no flush is needed.
+
+e2e: the same K steps driven step by step through the public C ABI with host
+buffers: mm_cd_step(amp from host), mm_cd_record, and a D2H copy of that
+step's receiver samples into pinned host memory every step.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, its
+sources compiled unmodified; run() with Target::Parallel and all host
+threads) on the same workload for a bounded sample of steps.  Under torchrun
+only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Gpoints/s (grid-point updates/sec) acoustic_iso_cd 8th-order"
+UNIT = "Gpoints/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--grid", type=int, default=None, help="cube edge (default: config per N)")
+    ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
+    ap.add_argument("--radius", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ model
+def byte_model(n, nd, r=4):
+    """Algorithmic bytes per step: 16 B/pt + 16 B per
+    damped-axis point (psi and zeta read + write)."""
+    N = float(n[0]) * n[1] * n[2]
+    damped = sum(N * 2 * nd[a] / n[a] for a in range(3))
+    return 16.0 * N + 16.0 * damped, N, damped
+
+
+def update_kernel_bytes(n, nd):
+    """Algorithmic bytes of one launch of the fused update kernel: p_cur,
+    p_prev, c read + p_next write (16 B/pt) + per damped-axis point psi read
+    and zeta read+write (12 B)."""
+    N = float(n[0]) * n[1] * n[2]
+    damped = sum(N * 2 * nd[a] / n[a] for a in range(3))
+    return 16.0 * N + 12.0 * damped
+
+
+def pass1_kernel_bytes(n, nd):
+    """pass 1: per damped-axis point psi read+write (8 B) + p_cur read once
+    per damped point (4 B)."""
+    N = float(n[0]) * n[1] * n[2]
+    damped = sum(N * 2 * nd[a] / n[a] for a in range(3))
+    inner = np.prod([n[a] - 2 * nd[a] for a in range(3)])
+    return 8.0 * damped + 4.0 * (N - inner)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if len(s) > 4 + k and s[4 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    """dram bytes per launch of the update kernel from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(workload, {}).get("update_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_reference_run(n, nsteps, nthreads):
+    from oracle.oracle import Oracle, available, nproc
+    kind = "reference" if available("reference") else "port"
+    o = Oracle(kind)
+    vp, vmin, vmax = o.layered_model(n)
+    if kind == "reference":
+        out = o.run(n, vp, nsteps=nsteps, nthreads=nthreads)
+        threads = nthreads
+    else:
+        out = o.run(n, vp, nsteps=nsteps)
+        threads = 1
+    gpts = n[0] * n[1] * n[2] * nsteps / out["kernel_seconds"] / 1e9
+    return gpts, kind, threads, out["kernel_seconds"]
+
+
+def cpu_sample_steps(n, requested):
+    if requested:
+        return requested
+    pts = n[0] * n[1] * n[2]
+    # ~0.1-0.2 Gpts/s on a multi-core host: aim at ~10-20 s of CPU work
+    return max(2, min(100, int(2.0e9 / pts)))
+
+
+# ------------------------------------------------------------------ our arm
+def default_grid(world):
+    return 240 if world == 1 else 512
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        from paper_2007_06048_b200 import dist as mmdist
+        return mmdist.bench_rank(args, rank, world, local)
+    import torch
+    import paper_2007_06048_b200 as mm
+    from paper_2007_06048_b200 import _lib
+
+    edge = args.grid or default_grid(world)
+    n = (edge, edge, edge)
+    r = args.radius
+    nd = (27, 27, 27)
+    torch.cuda.set_device(local)
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0), r)
+    model = mm.default_layered_model(grid)
+    dt = mm.cfl_dt(model, grid, 0.8)
+    total = args.warmup + args.steps
+    w = mm.ricker(25.0, dt, total).samples
+    src = tuple(x // 2 for x in n)
+    eng = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp,
+                              mm.EngineOptions(ndamping=nd, taper=True), dt, model.vmax,
+                              device=local, mode=args.mode)
+    geo = mm.default_receivers(grid, nd)
+    eng.set_receivers(geo.receivers, total)
+    ext = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
+
+    # warm-up (untimed) through the same device loop
+    eng.run(w[:args.warmup], src, record=True, first_sample=0)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.kernel_launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(ext)
+    eng.run(w[args.warmup:total], src, record=True, first_sample=args.warmup)
+    t1.record(ext)
+    t1.synchronize()
+    torch.cuda.synchronize()
+    launches = _lib.kernel_launch_count() - launches0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    pts = float(n[0]) * n[1] * n[2]
+    value = pts * args.steps / (ms * 1e-3) / 1e9
+
+    # per-kernel durations (dominant kernel = the fused update) over K steps
+    k_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for s in range(args.steps):
+        ev = k_ev[s]
+        ev[0].record(ext)
+        eng.update_boundary_psi()
+        ev[1].record(ext)
+        eng.update_planes(0, n[2])
+        ev[2].record(ext)
+        eng.inject_source(float(w[s % total]), src)
+        eng.rotate()
+        ev[3].record(ext)
+    torch.cuda.synchronize()
+    pass1_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in k_ev)
+    upd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in k_ev)
+
+    # e2e through the public API with host buffers
+    eng2 = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp,
+                               mm.EngineOptions(ndamping=nd, taper=True), dt, model.vmax,
+                               device=local, mode=args.mode)
+    eng2.set_receivers(geo.receivers, total)
+    nrec = geo.nreceivers()
+    host_out = torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
+    for s in range(args.warmup):
+        eng2.step(float(w[s]), src)
+        eng2.record(s)
+    eng2.synchronize()
+    ext2 = torch.cuda.ExternalStream(eng2.stream_handle(), device=local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    e0.record(ext2)
+    for s in range(args.warmup, total):
+        eng2.step(float(w[s]), src)       # 4 B of input per step (the source sample)
+        eng2.record(s)
+        eng2.copy_trace_step(s, host_out[s - args.warmup], asynchronous=True)
+    e1.record(ext2)
+    eng2.synchronize()
+    wall = time.perf_counter() - wall0
+    e2e_ms = max(e0.elapsed_time(e1), wall * 1e3)
+    e2e = pts * args.steps / (e2e_ms * 1e-3) / 1e9
+
+    peak, peak_src = measured_peak()
+    upd_bytes = update_kernel_bytes(n, nd)
+    achieved = upd_bytes / (upd_ms * 1e-3) / 1e9
+    step_bytes, _, _ = byte_model(n, nd)
+    step_gbs = step_bytes * args.steps / (ms * 1e-3) / 1e9
+    traffic = ncu_traffic(f"{edge}^3")
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (default two-layer vp model 1500/4500, Ricker source)",
+        "config": {"workload": f"acoustic_iso_cd r={r} {edge}^3 grid, nd=27 CPML, taper, "
+                               f"{nrec} surface receivers (BASELINE configs[1])",
+                   "grid": list(n), "radius": r, "ndamping": list(nd), "mode": args.mode,
+                   "l2": "working set (3 p fields + c + CPML) > 126 MB L2; no flush"},
+        "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": 4 * nrec},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "kernel": "update (inner + CPML pass 2)",
+                     "algorithmic_bytes_per_launch": upd_bytes,
+                     "kernel_ms": round(upd_ms, 4), "peak_source": peak_src},
+        "step_roofline": {"bytes_per_step_model": step_bytes,
+                          "achieved_gbs": round(step_gbs, 1),
+                          "frac": round(step_gbs / peak, 4),
+                          "roofline_gpts": round(peak * 1e9 / (step_bytes / pts) / 1e9, 1),
+                          "pass1_ms": round(pass1_ms, 4), "update_ms": round(upd_ms, 4)},
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        ns = cpu_sample_steps(n, args.cpu_sample_steps)
+        from oracle.oracle import nproc
+        cores = nproc()
+        gpts, kind, threads, secs = cpu_reference_run(n, ns, cores)
+        line["cpu_baseline"] = {"value": round(gpts, 5), "unit": UNIT, "cores": threads,
+                                "kind": kind,
+                                "sample": f"{edge}^3 x {ns} steps from t=0 ({secs:.1f} s), "
+                                          "run() Target::Parallel"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    edge = args.grid or default_grid(world)
+    n = (edge, edge, edge)
+    from oracle.oracle import nproc
+    cores = nproc()
+    ns = max(1, min(args.steps, cpu_sample_steps(n, args.cpu_sample_steps)))
+    # warm-up: one short run (page in, thread start-up)
+    cpu_reference_run(n, max(1, min(args.warmup, 2)), cores)
+    gpts, kind, threads, secs = cpu_reference_run(n, ns, cores)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gpts, 5), "unit": UNIT,
+        "n_gpus": world, "steps": ns, "warmup": args.warmup,
+        "ms_per_step": secs * 1e3 / ns, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (default two-layer model)",
+        "config": {"workload": f"acoustic_iso_cd r=4 {edge}^3 grid, nd=27 CPML, taper "
+                               f"(bounded sample: {ns} steps from t=0)", "grid": list(n)},
+        "cpu_baseline": {"value": round(gpts, 5), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{edge}^3 x {ns} steps, run() Target::Parallel"},
+        "e2e": {"value": round(gpts, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,237 @@
+/*
+ * minimod_b200.h -- C ABI of the B200-native acoustic_iso_cd propagator.
+ *
+ * Drop-in boundary for the reference's minimod::AcousticCdEngine<float>
+ * (/root/reference/proj/core/include/minimod/propagator.hpp:93-140,
+ * implemented at propagator_impl.hpp:53-173) and its callers run()
+ * (driver.cpp:83-144) and run_distributed_rank() (dist.cpp:144-267).
+ * Plain pointers and sizes only; no CUDA or torch types cross this boundary
+ * (streams are passed as void*).
+ *
+ * Conventions
+ *  - Every function returns an mm_status; on failure mm_last_error() holds a
+ *    thread-local message.  Status codes mirror the reference exceptions
+ *    (errors.hpp:10-30): ConfigError -> MM_ECONFIG, ValidationError ->
+ *    MM_EVALIDATION, InstabilityError -> MM_EINSTABILITY (step in
+ *    mm_last_instability_step()), std::invalid_argument -> MM_EINVAL.
+ *  - Host field arrays use the reference layout: ghosted, z fastest,
+ *    offset(i,j,k) = ((i+r)*(ny+2r) + (j+r))*(nz+2r) + (k+r)
+ *    (grid.hpp:61-65); (nx+2r)*(ny+2r)*(nz+2r) floats.
+ *  - Host pointers are caller-owned and only touched during the call.  The
+ *    engine owns all device memory.  One host thread drives one engine at a
+ *    time; calls are not reentrant (same rule as the reference).
+ *  - Engine calls are asynchronous on the engine's CUDA stream except those
+ *    that return host data (get_*) and mm_cd_synchronize.
+ */
+#ifndef MINIMOD_B200_H
+#define MINIMOD_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mm_status {
+    MM_OK = 0,
+    MM_ECONFIG = 1,      /* minimod::ConfigError */
+    MM_EVALIDATION = 2,  /* minimod::ValidationError */
+    MM_EINSTABILITY = 3, /* minimod::InstabilityError */
+    MM_EINVAL = 4,       /* std::invalid_argument / contract violation */
+    MM_ECUDA = 5,        /* CUDA runtime failure */
+    MM_ENCCL = 6         /* collective failure (multi-GPU plumbing) */
+} mm_status;
+
+/* Arithmetic modes of the device step.
+ *  MM_MODE_STRICT: reference association order, no FMA contraction;
+ *                  bit-identical to the CPU reference.
+ *  MM_MODE_FAST:   the TMA/register-queue kernels (default). */
+typedef enum mm_mode { MM_MODE_FAST = 0, MM_MODE_STRICT = 1 } mm_mode;
+
+/* ref: grid.hpp:49-73 Grid3D (n, d, radius; stagger is not used by CD). */
+typedef struct mm_grid {
+    int n[3];
+    double d[3];
+    int radius;
+} mm_grid;
+
+/* ref: propagator.hpp:23-30 EngineOptions (defaults: ndamping 0, fmax 25,
+ * r_target 1e-3, free_surface 0, taper 0, ntaper 3). */
+typedef struct mm_engine_options {
+    int ndamping[3];
+    double fmax;
+    double r_target;
+    int free_surface;
+    int taper;
+    int ntaper[3];
+} mm_engine_options;
+
+typedef struct mm_cd_engine mm_cd_engine;
+
+const char* mm_last_error(void);
+int mm_last_instability_step(void);
+const char* mm_version(void);
+/* Number of CUDA devices visible (0 on a CPU-only host). */
+int mm_device_count(int* count);
+/* Kernel launches issued by this process so far (all engines). */
+long long mm_kernel_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * Host numerics (C++; bit-identical to the reference)
+ * --------------------------------------------------------------------- */
+
+/* ref: stencil.cpp:50-74 second_derivative_coeffs -> c[radius] (1/h^2 folded
+ * in) and the center weight. */
+int mm_second_derivative_coeffs(int radius, double h, double* c, double* center);
+/* ref: stencil.cpp:99-117 central_first_derivative_coeffs -> c[radius]. */
+int mm_central_first_derivative_coeffs(int radius, double h, double* c);
+/* ref: driver.cpp:19-29 cfl_dt. */
+int mm_cfl_dt(double vmax, const mm_grid* grid, double cfl, double* dt);
+/* ref: source.cpp:11-28 ricker. */
+int mm_ricker(double fmax, double dt, int nsteps, float* out);
+/* ref: cpml.hpp:34-72 build_profile<float>.  a/b/inv_kappa are the three
+ * axes concatenated (n[0]+n[1]+n[2] floats each); d0[3] optional. */
+int mm_build_profile(const int n[3], const double h[3], const int ndamping[3], double fmax,
+                     double vmax, double dt, double r_target, int free_surface, float* a,
+                     float* b, float* inv_kappa, double* d0);
+/* ref: propagator.hpp:36-62 taper_material (then fill_ghosts_replicate), in
+ * place on a ghosted z-fastest field. */
+int mm_taper_material(float* f, const int n[3], int radius, const int ntaper[3],
+                      const int offset[3], const int global_n[3]);
+/* ref: model.cpp:63-77 default_layered_model (vp only) + validate_model. */
+int mm_layered_model(const int n[3], int radius, float* vp, float* vmin, float* vmax);
+/* ref: model.cpp:15-43 validate_model for vp: checks finite and > 0,
+ * computes vmin/vmax, replicates ghosts in place. */
+int mm_validate_model(const int n[3], int radius, float* vp, float* vmin, float* vmax);
+
+/* ------------------------------------------------------------------------
+ * Engine (ref: AcousticCdEngine<float>)
+ * --------------------------------------------------------------------- */
+
+/* ref: propagator.hpp:96-98 ctor.  vp_local: ghosted z-fastest local field
+ * (copied).  offset/global_n place the local box in the global grid (0 and
+ * local n for single-device use).  device: CUDA ordinal; mode: mm_mode. */
+int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3],
+                 const float* vp_local, const mm_engine_options* opts, float dt,
+                 double vmax_global, int device, int mode, mm_cd_engine** out);
+int mm_cd_destroy(mm_cd_engine* e);
+
+/* ref: propagator.hpp:103-104 step(amp, src).  src_local: 3 ints in local
+ * interior coordinates, or NULL when this engine does not own the source. */
+int mm_cd_step(mm_cd_engine* e, float amp, const int* src_local);
+
+/* Sub-phases of one step, in the reference order (propagator_impl.hpp:
+ * 154-173).  Calling them in this order equals mm_cd_step. */
+int mm_cd_update_boundary_psi(mm_cd_engine* e); /* pass 1, :106-123 */
+int mm_cd_update_inner(mm_cd_engine* e);        /* update_plain, :89-104 */
+int mm_cd_update_boundary(mm_cd_engine* e);     /* pass 2, :125-152 */
+int mm_cd_inject_source(mm_cd_engine* e, float amp, const int* src_local); /* :166-169 */
+int mm_cd_apply_free_surface(mm_cd_engine* e);  /* :170, cpml.hpp:103-111 */
+int mm_cd_rotate(mm_cd_engine* e);              /* :171-172 */
+
+int mm_cd_synchronize(mm_cd_engine* e);
+/* Number of floats in one ghosted local field (host layout). */
+int mm_cd_field_size(mm_cd_engine* e, size_t* count);
+int mm_cd_get_dt(mm_cd_engine* e, float* dt);
+int mm_cd_get_mode(mm_cd_engine* e, int* mode);
+int mm_cd_steps_taken(mm_cd_engine* e, long long* steps);
+
+/* ref: propagator.hpp:106-110 pressure()/pressure_prev() (device -> host,
+ * reference layout, ghosts included). */
+int mm_cd_get_pressure(mm_cd_engine* e, float* host);
+int mm_cd_get_pressure_prev(mm_cd_engine* e, float* host);
+/* Tapered vp copy the engine steps with (ref: propagator_impl.hpp:60,73). */
+int mm_cd_get_velocity(mm_cd_engine* e, float* host);
+/* ref: propagator.hpp:116-120 set_state(p_prev, p_cur). */
+int mm_cd_set_state(mm_cd_engine* e, const float* p_prev, const float* p_cur);
+
+/* ref: propagator.hpp:112-114 profile().  Tables over the GLOBAL axis
+ * length global_n[axis].  set_profile replaces the tables; it is accepted
+ * before the first step only, and a must be zero outside the damping
+ * layers (the CPML memory lives only there). */
+int mm_cd_get_profile(mm_cd_engine* e, int axis, float* a, float* b, float* inv_kappa);
+int mm_cd_set_profile(mm_cd_engine* e, int axis, const float* a, const float* b,
+                      const float* inv_kappa);
+int mm_cd_get_d0(mm_cd_engine* e, double d0[3]);
+
+/* Receiver hooks (ref: source.cpp:40-66 default_receivers/record,
+ * source.hpp:44-52 ShotRecord).  ijk: n receivers x 3 local interior
+ * coordinates.  capacity: number of time samples the device trace buffer
+ * holds.  mm_cd_record(step) samples p_cur into column `step`.
+ * mm_cd_get_traces copies out in ShotRecord layout traces[r*nsteps + s]. */
+int mm_cd_set_receivers(mm_cd_engine* e, const int* ijk, int nreceivers, int capacity);
+int mm_cd_record(mm_cd_engine* e, int step);
+int mm_cd_get_traces(mm_cd_engine* e, float* host, int nsteps);
+/* Copy one recorded time sample (all receivers, nreceivers floats, receiver
+ * order) to host memory.  async != 0: enqueue on the engine stream and
+ * return (host should be pinned; read it after mm_cd_synchronize). */
+int mm_cd_copy_trace_step(mm_cd_engine* e, int step, float* host, int async);
+
+/* Device-resident time loop: nsteps steps with source amplitudes amps[]
+ * (device copy), recording every step into columns [first_sample, ...) when
+ * record != 0, one receiver-0 finiteness check per step (ref: driver.cpp:
+ * 102-112,68-71).  CUDA-graph captured.  *device_ms (optional) = device
+ * time of the loop (CUDA events).  Returns MM_EINSTABILITY with the first
+ * failing step (1-based, as the reference) if receiver 0 went non-finite. */
+int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src_local, int record,
+              int first_sample, float* device_ms);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU plumbing (z-slabs; ref: dist.cpp:92-115 exchange_halos).
+ * The halo transport itself (NCCL send/recv) is issued by the host runtime
+ * on the engine's stream; these expose the contiguous plane ranges.
+ * --------------------------------------------------------------------- */
+/* CUDA stream (cudaStream_t) the engine launches on. */
+int mm_cd_stream(mm_cd_engine* e, void** stream);
+/* Device pointer + byte size of the r z-planes of p_cur on one side:
+ * side 0 = low z, 1 = high z; which 0 = owned edge planes (send),
+ * 1 = ghost planes (receive).  The device layout is z slowest, so each
+ * range is one contiguous block. */
+int mm_cd_halo_planes(mm_cd_engine* e, int side, int which, void** dev_ptr, size_t* bytes);
+/* Same for p_next (the field the current step is writing). */
+int mm_cd_next_halo_planes(mm_cd_engine* e, int side, int which, void** dev_ptr, size_t* bytes);
+/* Restricted step pieces for overlap: compute p_next on local planes
+ * [z_lo, z_hi) only (both CPML passes and the inner update). */
+int mm_cd_update_planes(mm_cd_engine* e, int z_lo, int z_hi);
+
+/* ------------------------------------------------------------------------
+ * Driver (ref: driver.cpp:83-144 run(), acoustic_iso_cd only)
+ * --------------------------------------------------------------------- */
+typedef struct mm_sim_config {
+    int ngrid[3];
+    double dgrid[3];
+    int nsteps;
+    double fmax;
+    double cfl;
+    int ndamping[3];
+    int ntaper[3];
+    int taper;
+    int free_surface;
+    double r_target;
+    int has_source_loc;
+    int source_loc[3];
+    int receiver_increment[2];
+    int stencil_radius;
+} mm_sim_config;
+
+typedef struct mm_run_report {
+    double dt;
+    double kernel_seconds;   /* device time of the step loop */
+    double modeling_seconds; /* wall time of the whole run */
+    int steps_run;
+    int nreceivers;
+} mm_run_report;
+
+/* Fills *cfg with the reference SimConfig defaults (driver.hpp:21-47). */
+int mm_sim_config_default(mm_sim_config* cfg);
+/* vp_model: ghosted z-fastest model (validated/replicated here).  traces:
+ * nreceivers*nsteps floats (NULL to skip the copy-out); nreceivers of the
+ * default carpet = ceil(nx/inc0)*ceil(ny/inc1). */
+int mm_run(const mm_sim_config* cfg, const float* vp_model, int device, int mode, float* traces,
+           mm_run_report* report);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* MINIMOD_B200_H */

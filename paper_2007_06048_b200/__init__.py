@@ -1,0 +1,28 @@
+"""minimod-b200: B200-native acoustic_iso_cd propagator (Minimod, arXiv 2007.06048).
+
+Python front-end over the C-ABI CUDA library ``libminimod_b200.so``
+(include/minimod_b200.h).  Mirrors the reference's engine/driver interface:
+``AcousticCdEngine``, ``EngineOptions``, ``SimConfig``, ``run``, ``cfl_dt``,
+``ricker``, ``default_layered_model`` ....
+"""
+from ._lib import (CollectiveError, ConfigError, CudaError, InstabilityError, MinimodError,
+                   ValidationError, device_count, kernel_launch_count)
+from .driver import RunReport, SimConfig, build_geometry, cfl_dt, run
+from .numerics import (AcquisitionGeometry, AxisCpml, CpmlProfile, EarthModel, Grid3D, IndexBox,
+                       RegionPartition, ShotRecord, StencilCoeffs, Wavelet, build_profile,
+                       central_first_derivative_coeffs, constant_model, default_layered_model,
+                       default_receivers, fill_ghosts_replicate, intersect, make_grid,
+                       partition_regions, random_model, ricker, second_derivative_coeffs,
+                       taper_material, validate_model, version)
+from .propagator import AcousticCdEngine, EngineOptions
+
+__all__ = [
+    "AcousticCdEngine", "EngineOptions", "SimConfig", "RunReport", "run", "cfl_dt",
+    "build_geometry", "Grid3D", "IndexBox", "RegionPartition", "make_grid", "partition_regions",
+    "intersect", "fill_ghosts_replicate", "StencilCoeffs", "second_derivative_coeffs",
+    "central_first_derivative_coeffs", "AxisCpml", "CpmlProfile", "build_profile",
+    "taper_material", "EarthModel", "validate_model", "constant_model", "default_layered_model",
+    "random_model", "Wavelet", "ricker", "AcquisitionGeometry", "default_receivers",
+    "ShotRecord", "ConfigError", "ValidationError", "InstabilityError", "CudaError",
+    "CollectiveError", "MinimodError", "device_count", "kernel_launch_count", "version",
+]

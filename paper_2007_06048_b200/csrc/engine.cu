@@ -1,0 +1,920 @@
+// engine.cu -- the AcousticCdEngine drop-in behind the C ABI (include/minimod_b200.h).
+//
+// Mirrors minimod::AcousticCdEngine<float> (propagator.hpp:93-140,
+// propagator_impl.hpp:53-173): the constructor does the same setup on the
+// host (weights, CPML profile with the float-rounded dt, material taper,
+// region partition), uploads the fields in the device layout of
+// mm_internal.hpp and from then on every step runs on the GPU.  The three
+// pressure buffers rotate by index exactly as the reference swaps
+// p_prev/p_cur/p_next, so ghost contents (zero, free-surface mirror or halo
+// planes) behave identically.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/minimod_b200.h"
+#include "mm_fast.hpp"
+#include "mm_internal.hpp"
+
+namespace mmb {
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_step = 0;
+std::atomic<long long> g_launches{0};
+}  // namespace
+
+void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        throw Error(ST_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what +
+                               " (" + file + ":" + std::to_string(line) + ")");
+}
+
+Layout Layout::make(const int n[3], int r) {
+    Layout l;
+    for (int a = 0; a < 3; ++a) l.n[a] = n[a];
+    l.r = r;
+    l.L = (r + 3) / 4 * 4;
+    l.P = (l.L + n[0] + r + 31) / 32 * 32;
+    l.ey = n[1] + 2 * r;
+    l.ez = n[2] + 2 * r;
+    l.plane = (long long)l.ey * l.P;
+    l.total = l.plane * l.ez;
+    return l;
+}
+
+template <typename T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        count = 0;
+    }
+    void alloc(size_t n) {
+        reset();
+        if (n == 0) return;
+        MM_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+        count = n;
+    }
+    void alloc_zero(size_t n, cudaStream_t s) {
+        alloc(n);
+        if (n) MM_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));
+    }
+    void upload(const T* host, size_t n, cudaStream_t s) {
+        if (count < n) alloc(n);
+        if (n) MM_CUDA(cudaMemcpyAsync(ptr, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
+}  // namespace mmb
+
+using namespace mmb;
+
+struct mm_cd_engine {
+    int device = 0;
+    int mode = MM_MODE_FAST;
+    cudaStream_t stream = nullptr;
+    Layout lay;
+    HostGrid hg;
+    int goff[3], gn[3], nd[3];
+    double d[3];
+    bool free_surface = false;
+    float dt = 0, dt2 = 0;
+    Profile prof;
+    float c2[3][kMaxR] = {};
+    float c1[3][kMaxR] = {};
+    DevBuf<float> p[3];
+    int ip = 0, ic = 1, in = 2;  // prev / cur / next buffer indices
+    DevBuf<float> cv, vp;
+    // CPML
+    DevBuf<float> ta[3], tb[3], tik[3];
+    DevBuf<int> map[3], list[3];
+    int cnt[3] = {0, 0, 0};
+    DevBuf<float> psi[3], zeta[3];
+    long long cs1[3] = {0, 0, 0}, cs2[3] = {0, 0, 0};
+    // receivers / driver
+    std::vector<int> rec_ijk;
+    DevBuf<long long> rec_offs;
+    DevBuf<float> traces;
+    int nrec = 0, cap = 0;
+    DevBuf<int> counters;  // [0] step counter, [1] first bad step
+    DevBuf<float> amps;
+    long long steps = 0;
+    std::unique_ptr<FastPlan> fast;
+
+    StepParams params() const {
+        StepParams s;
+        std::memset(&s, 0, sizeof s);
+        s.lay = lay;
+        for (int a = 0; a < 3; ++a) {
+            s.goff[a] = goff[a];
+            s.gn[a] = gn[a];
+            s.nd[a] = nd[a];
+            s.ta[a] = ta[a].ptr;
+            s.tb[a] = tb[a].ptr;
+            s.tik[a] = tik[a].ptr;
+            s.map[a] = map[a].ptr;
+            s.list[a] = list[a].ptr;
+            s.cnt[a] = cnt[a];
+            s.psi[a] = psi[a].ptr;
+            s.zeta[a] = zeta[a].ptr;
+            s.cs1[a] = cs1[a];
+            s.cs2[a] = cs2[a];
+            for (int m = 0; m < kMaxR; ++m) {
+                s.c2[a][m] = c2[a][m];
+                s.c1[a][m] = c1[a][m];
+            }
+        }
+        s.pc = p[ic].ptr;
+        s.pp = p[ip].ptr;
+        s.pn = p[in].ptr;
+        s.cv = cv.ptr;
+        return s;
+    }
+
+    // Local tables + active-index maps + compact CPML storage from prof.
+    void setup_cpml() {
+        for (int ax = 0; ax < 3; ++ax) {
+            const int n = lay.n[ax];
+            std::vector<float> a(n), b(n), k(n);
+            std::vector<int> mp(n, -1), ls;
+            for (int l = 0; l < n; ++l) {
+                const int g = l + goff[ax];
+                a[l] = prof.a[ax][g];
+                b[l] = prof.b[ax][g];
+                k[l] = prof.ik[ax][g];
+                if (a[l] != 0.0f) {
+                    mp[l] = (int)ls.size();
+                    ls.push_back(l);
+                }
+            }
+            cnt[ax] = (int)ls.size();
+            ta[ax].upload(a.data(), n, stream);
+            tb[ax].upload(b.data(), n, stream);
+            tik[ax].upload(k.data(), n, stream);
+            map[ax].upload(mp.data(), n, stream);
+            if (ls.empty()) ls.push_back(0);  // keep a valid pointer
+            list[ax].upload(ls.data(), ls.size(), stream);
+        }
+        const long long nx4 = (lay.n[0] + 3) / 4 * 4;
+        const long long w0 = (cnt[0] + 3) / 4 * 4;
+        cs1[0] = w0;
+        cs2[0] = w0 * lay.n[1];
+        cs1[1] = nx4;
+        cs2[1] = nx4 * cnt[1];
+        cs1[2] = nx4;
+        cs2[2] = nx4 * lay.n[1];
+        const size_t sz[3] = {(size_t)(cnt[0] ? cs2[0] * lay.n[2] : 0),
+                              (size_t)(cnt[1] ? cs2[1] * lay.n[2] : 0),
+                              (size_t)(cnt[2] ? cs2[2] * cnt[2] : 0)};
+        for (int ax = 0; ax < 3; ++ax) {
+            psi[ax].alloc_zero(sz[ax], stream);
+            zeta[ax].alloc_zero(sz[ax], stream);
+        }
+    }
+
+    void rotate() {
+        const int t = ip;
+        ip = ic;
+        ic = in;
+        in = t;
+    }
+
+    long long src_off(const int* src) const {
+        for (int a = 0; a < 3; ++a)
+            if (src[a] < 0 || src[a] >= lay.n[a])
+                raise(ST_CONFIG, "source location outside grid interior");
+        return lay.off(src[0], src[1], src[2]);
+    }
+
+    void pass1() {
+        const StepParams s = params();
+        if (mode == MM_MODE_STRICT || !fast)
+            strict_pass1(s, 0, lay.n[2], stream);
+        else
+            fast->pass1(s, stream);
+    }
+    void update(int region, int z_lo, int z_hi) {
+        const StepParams s = params();
+        if (mode == MM_MODE_STRICT || !fast)
+            strict_update(s, region, z_lo, z_hi, stream);
+        else
+            fast->update(s, region, z_lo, z_hi, stream);
+    }
+    void finish_step(float amp, const int* src, const float* amp_dev, const int* step_dev) {
+        if (src) launch_inject(p[in].ptr, cv.ptr, src_off(src), amp, amp_dev, step_dev, stream);
+        if (free_surface && goff[2] == 0) launch_free_surface(p[in].ptr, lay, stream);
+        rotate();
+        ++steps;
+    }
+    void full_step(float amp, const int* src, const float* amp_dev, const int* step_dev) {
+        if (mode != MM_MODE_STRICT && fast) {
+            fast->step(params(), src ? src_off(src) : -1LL, amp, amp_dev, step_dev, stream);
+            if (free_surface && goff[2] == 0) launch_free_surface(p[in].ptr, lay, stream);
+            rotate();
+            ++steps;
+            return;
+        }
+        pass1();
+        update(0, 0, lay.n[2]);
+        finish_step(amp, src, amp_dev, step_dev);
+    }
+
+    void to_host(const float* dev, float* host) {
+        DevBuf<float> stage;
+        stage.alloc(hg.volume());
+        launch_to_host_layout(dev, stage.ptr, lay, stream);
+        MM_CUDA(cudaMemcpyAsync(host, stage.ptr, hg.volume() * sizeof(float),
+                                cudaMemcpyDeviceToHost, stream));
+        MM_CUDA(cudaStreamSynchronize(stream));
+    }
+    void from_host(const float* host, float* dev) {
+        DevBuf<float> stage;
+        stage.upload(host, hg.volume(), stream);
+        launch_to_device_layout(stage.ptr, dev, lay, stream);
+        MM_CUDA(cudaStreamSynchronize(stream));
+    }
+
+    ~mm_cd_engine() {
+        if (stream) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(stream);
+        }
+        fast.reset();
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+int set_error(int code, const std::string& msg, int step = 0) {
+    g_err = msg;
+    g_step = step;
+    return code;
+}
+
+#define MM_API_BEGIN try {
+#define MM_API_END                                                       \
+    }                                                                    \
+    catch (const mmb::Error& ex) {                                       \
+        return set_error(ex.code, ex.what(), ex.step);                   \
+    }                                                                    \
+    catch (const std::bad_alloc&) {                                      \
+        return set_error(MM_EINVAL, "host allocation failed");           \
+    }                                                                    \
+    catch (const std::exception& ex) {                                   \
+        return set_error(MM_EINVAL, ex.what());                          \
+    }                                                                    \
+    return MM_OK;
+
+void need(const void* p, const char* what) {
+    if (!p) raise(ST_INVAL, std::string(what) + " must not be NULL");
+}
+
+void use(mm_cd_engine* e) {
+    need(e, "engine");
+    MM_CUDA(cudaSetDevice(e->device));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mm_last_error(void) { return g_err.c_str(); }
+int mm_last_instability_step(void) { return g_step; }
+const char* mm_version(void) { return "minimod-b200 0.1 (sm_100a)"; }
+long long mm_kernel_launch_count(void) { return g_launches.load(); }
+
+int mm_device_count(int* count) {
+    MM_API_BEGIN
+    need(count, "count");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *count = c;
+    MM_API_END
+}
+
+int mm_second_derivative_coeffs(int radius, double h, double* c, double* center) {
+    MM_API_BEGIN
+    need(c, "c");
+    const Coeffs k = second_derivative(radius, h);
+    for (int m = 0; m < radius; ++m) c[m] = k.c[m];
+    if (center) *center = k.center;
+    MM_API_END
+}
+
+int mm_central_first_derivative_coeffs(int radius, double h, double* c) {
+    MM_API_BEGIN
+    need(c, "c");
+    const Coeffs k = central_first_derivative(radius, h);
+    for (int m = 0; m < radius; ++m) c[m] = k.c[m];
+    MM_API_END
+}
+
+int mm_cfl_dt(double vmax, const mm_grid* grid, double cfl, double* dt) {
+    MM_API_BEGIN
+    need(grid, "grid");
+    need(dt, "dt");
+    *dt = cfl_dt(vmax, grid->n, grid->d, grid->radius, cfl);
+    MM_API_END
+}
+
+int mm_ricker(double fmax, double dt, int nsteps, float* out) {
+    MM_API_BEGIN
+    const std::vector<float> w = ricker(fmax, dt, nsteps);
+    if (nsteps > 0) {
+        need(out, "out");
+        std::memcpy(out, w.data(), sizeof(float) * w.size());
+    }
+    MM_API_END
+}
+
+int mm_build_profile(const int n[3], const double h[3], const int nd[3], double fmax, double vmax,
+                     double dt, double r_target, int free_surface, float* a, float* b,
+                     float* inv_kappa, double* d0) {
+    MM_API_BEGIN
+    need(n, "n");
+    need(h, "h");
+    need(nd, "ndamping");
+    const Profile p = build_profile(n, h, nd, fmax, vmax, dt, r_target, free_surface != 0);
+    size_t o = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+        if (a) std::memcpy(a + o, p.a[ax].data(), sizeof(float) * n[ax]);
+        if (b) std::memcpy(b + o, p.b[ax].data(), sizeof(float) * n[ax]);
+        if (inv_kappa) std::memcpy(inv_kappa + o, p.ik[ax].data(), sizeof(float) * n[ax]);
+        if (d0) d0[ax] = p.d0[ax];
+        o += n[ax];
+    }
+    MM_API_END
+}
+
+int mm_taper_material(float* f, const int n[3], int radius, const int ntaper[3],
+                      const int offset[3], const int global_n[3]) {
+    MM_API_BEGIN
+    need(f, "f");
+    const HostGrid g{{n[0], n[1], n[2]}, radius};
+    taper_material(f, g, ntaper, offset, global_n);
+    MM_API_END
+}
+
+int mm_layered_model(const int n[3], int radius, float* vp, float* vmin, float* vmax) {
+    MM_API_BEGIN
+    need(vp, "vp");
+    const HostGrid g{{n[0], n[1], n[2]}, radius};
+    std::fill(vp, vp + g.volume(), 0.0f);
+    const int half = n[2] / 2;
+    for (int i = 0; i < n[0]; ++i)
+        for (int j = 0; j < n[1]; ++j)
+            for (int k = 0; k < n[2]; ++k) vp[g.off(i, j, k)] = k < half ? 1500.0f : 4500.0f;
+    validate_vp(vp, g, vmin, vmax);
+    fill_ghosts_replicate(vp, g);
+    MM_API_END
+}
+
+int mm_validate_model(const int n[3], int radius, float* vp, float* vmin, float* vmax) {
+    MM_API_BEGIN
+    need(vp, "vp");
+    const HostGrid g{{n[0], n[1], n[2]}, radius};
+    validate_vp(vp, g, vmin, vmax);
+    fill_ghosts_replicate(vp, g);
+    MM_API_END
+}
+
+int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3],
+                 const float* vp_local, const mm_engine_options* opts, float dt,
+                 double vmax_global, int device, int mode, mm_cd_engine** out) {
+    MM_API_BEGIN
+    need(local, "grid");
+    need(offset, "offset");
+    need(global_n, "global_n");
+    need(vp_local, "vp_local");
+    need(opts, "options");
+    need(out, "out");
+    *out = nullptr;
+    // make_grid validation (grid.cpp:5-22)
+    static const char* axn[3] = {"x", "y", "z"};
+    for (int a = 0; a < 3; ++a) {
+        if (local->n[a] < 1)
+            raise(ST_CONFIG, std::string("grid size must be >= 1 along ") + axn[a] + ", got " +
+                               std::to_string(local->n[a]));
+        if (!(local->d[a] > 0.0))
+            raise(ST_CONFIG, std::string("grid spacing must be > 0 along ") + axn[a]);
+    }
+    if (local->radius < 1 || local->radius > kMaxR)
+        raise(ST_CONFIG, "stencil radius must be in [1, 8], got " + std::to_string(local->radius));
+    if (mode != MM_MODE_FAST && mode != MM_MODE_STRICT) raise(ST_INVAL, "unknown mode");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        raise(ST_CUDA, "no CUDA device available: the acoustic_iso_cd engine runs on the GPU only");
+    }
+    if (device < 0 || device >= ndev) raise(ST_INVAL, "device ordinal out of range");
+    MM_CUDA(cudaSetDevice(device));
+
+    auto e = std::make_unique<mm_cd_engine>();
+    e->device = device;
+    e->mode = mode;
+    MM_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    e->lay = Layout::make(local->n, local->radius);
+    e->hg = HostGrid{{local->n[0], local->n[1], local->n[2]}, local->radius};
+    for (int a = 0; a < 3; ++a) {
+        e->goff[a] = offset[a];
+        e->gn[a] = global_n[a];
+        e->nd[a] = opts->ndamping[a];
+        e->d[a] = local->d[a];
+        if (offset[a] < 0 || offset[a] + local->n[a] > global_n[a])
+            raise(ST_CONFIG, "local box does not fit inside the global grid");
+    }
+    e->free_surface = opts->free_surface != 0;
+    e->dt = dt;
+    e->dt2 = dt * dt;
+    const int r = local->radius;
+    // weights (propagator_impl.hpp:67-70)
+    for (int ax = 0; ax < 3; ++ax) {
+        const Coeffs w2 = second_derivative(r, local->d[ax]);
+        const Coeffs w1 = central_first_derivative(r, local->d[ax]);
+        for (int m = 0; m < r; ++m) {
+            e->c2[ax][m] = static_cast<float>(w2.c[m]);
+            e->c1[ax][m] = static_cast<float>(w1.c[m]);
+        }
+    }
+    // CPML profile with the float-rounded dt (propagator_impl.hpp:71-72)
+    e->prof = build_profile(global_n, local->d, opts->ndamping, opts->fmax, vmax_global,
+                            static_cast<double>(dt), opts->r_target, e->free_surface);
+    // taper on the engine's own vp copy (propagator_impl.hpp:73)
+    std::vector<float> vp(vp_local, vp_local + e->hg.volume());
+    if (opts->taper) taper_material(vp.data(), e->hg, opts->ntaper, offset, global_n);
+    // region partition checks (grid.cpp:24-33)
+    for (int a = 0; a < 3; ++a) {
+        if (opts->ndamping[a] < 0) raise(ST_CONFIG, "ndamping must be >= 0");
+        if (2 * opts->ndamping[a] >= global_n[a])
+            raise(ST_CONFIG, std::string("damping layers too thick along ") + axn[a] + ": 2*" +
+                               std::to_string(opts->ndamping[a]) +
+                               " >= " + std::to_string(global_n[a]));
+    }
+    // device fields
+    const Layout& L = e->lay;
+    for (int b = 0; b < 3; ++b) e->p[b].alloc_zero(L.total, e->stream);
+    e->vp.alloc_zero(L.total, e->stream);
+    e->cv.alloc_zero(L.total, e->stream);
+    e->from_host(vp.data(), e->vp.ptr);
+    launch_velocity_coeff(e->vp.ptr, e->cv.ptr, e->dt2, L.total, e->stream);
+    e->setup_cpml();
+    e->counters.alloc_zero(2, e->stream);
+    if (mode == MM_MODE_FAST) e->fast = make_fast_plan(e->lay, device);
+    MM_CUDA(cudaStreamSynchronize(e->stream));
+    *out = e.release();
+    MM_API_END
+}
+
+int mm_cd_destroy(mm_cd_engine* e) {
+    MM_API_BEGIN
+    if (!e) return MM_OK;
+    cudaSetDevice(e->device);
+    delete e;
+    MM_API_END
+}
+
+int mm_cd_step(mm_cd_engine* e, float amp, const int* src) {
+    MM_API_BEGIN
+    use(e);
+    e->full_step(amp, src, nullptr, nullptr);
+    MM_API_END
+}
+
+int mm_cd_update_boundary_psi(mm_cd_engine* e) {
+    MM_API_BEGIN
+    use(e);
+    e->pass1();
+    MM_API_END
+}
+
+int mm_cd_update_inner(mm_cd_engine* e) {
+    MM_API_BEGIN
+    use(e);
+    e->update(1, 0, e->lay.n[2]);
+    MM_API_END
+}
+
+int mm_cd_update_boundary(mm_cd_engine* e) {
+    MM_API_BEGIN
+    use(e);
+    e->update(2, 0, e->lay.n[2]);
+    MM_API_END
+}
+
+int mm_cd_update_planes(mm_cd_engine* e, int z_lo, int z_hi) {
+    MM_API_BEGIN
+    use(e);
+    if (z_lo < 0 || z_hi > e->lay.n[2] || z_lo > z_hi) raise(ST_INVAL, "plane range out of bounds");
+    e->update(0, z_lo, z_hi);
+    MM_API_END
+}
+
+int mm_cd_inject_source(mm_cd_engine* e, float amp, const int* src) {
+    MM_API_BEGIN
+    use(e);
+    if (src) launch_inject(e->p[e->in].ptr, e->cv.ptr, e->src_off(src), amp, nullptr, nullptr,
+                           e->stream);
+    MM_API_END
+}
+
+int mm_cd_apply_free_surface(mm_cd_engine* e) {
+    MM_API_BEGIN
+    use(e);
+    if (e->free_surface && e->goff[2] == 0) launch_free_surface(e->p[e->in].ptr, e->lay, e->stream);
+    MM_API_END
+}
+
+int mm_cd_rotate(mm_cd_engine* e) {
+    MM_API_BEGIN
+    use(e);
+    e->rotate();
+    ++e->steps;
+    MM_API_END
+}
+
+int mm_cd_synchronize(mm_cd_engine* e) {
+    MM_API_BEGIN
+    use(e);
+    MM_CUDA(cudaStreamSynchronize(e->stream));
+    MM_API_END
+}
+
+int mm_cd_field_size(mm_cd_engine* e, size_t* count) {
+    MM_API_BEGIN
+    need(e, "engine");
+    need(count, "count");
+    *count = e->hg.volume();
+    MM_API_END
+}
+
+int mm_cd_get_dt(mm_cd_engine* e, float* dt) {
+    MM_API_BEGIN
+    need(e, "engine");
+    need(dt, "dt");
+    *dt = e->dt;
+    MM_API_END
+}
+
+int mm_cd_get_mode(mm_cd_engine* e, int* mode) {
+    MM_API_BEGIN
+    need(e, "engine");
+    need(mode, "mode");
+    *mode = e->mode;
+    MM_API_END
+}
+
+int mm_cd_steps_taken(mm_cd_engine* e, long long* steps) {
+    MM_API_BEGIN
+    need(e, "engine");
+    need(steps, "steps");
+    *steps = e->steps;
+    MM_API_END
+}
+
+int mm_cd_get_pressure(mm_cd_engine* e, float* host) {
+    MM_API_BEGIN
+    use(e);
+    need(host, "host");
+    e->to_host(e->p[e->ic].ptr, host);
+    MM_API_END
+}
+
+int mm_cd_get_pressure_prev(mm_cd_engine* e, float* host) {
+    MM_API_BEGIN
+    use(e);
+    need(host, "host");
+    e->to_host(e->p[e->ip].ptr, host);
+    MM_API_END
+}
+
+int mm_cd_get_velocity(mm_cd_engine* e, float* host) {
+    MM_API_BEGIN
+    use(e);
+    need(host, "host");
+    e->to_host(e->vp.ptr, host);
+    MM_API_END
+}
+
+int mm_cd_set_state(mm_cd_engine* e, const float* p_prev, const float* p_cur) {
+    MM_API_BEGIN
+    use(e);
+    need(p_prev, "p_prev");
+    need(p_cur, "p_cur");
+    e->from_host(p_prev, e->p[e->ip].ptr);
+    e->from_host(p_cur, e->p[e->ic].ptr);
+    MM_API_END
+}
+
+int mm_cd_get_profile(mm_cd_engine* e, int axis, float* a, float* b, float* inv_kappa) {
+    MM_API_BEGIN
+    need(e, "engine");
+    if (axis < 0 || axis > 2) raise(ST_INVAL, "axis must be 0, 1 or 2");
+    const size_t n = e->prof.a[axis].size();
+    if (a) std::memcpy(a, e->prof.a[axis].data(), n * sizeof(float));
+    if (b) std::memcpy(b, e->prof.b[axis].data(), n * sizeof(float));
+    if (inv_kappa) std::memcpy(inv_kappa, e->prof.ik[axis].data(), n * sizeof(float));
+    MM_API_END
+}
+
+int mm_cd_set_profile(mm_cd_engine* e, int axis, const float* a, const float* b,
+                      const float* inv_kappa) {
+    MM_API_BEGIN
+    use(e);
+    if (axis < 0 || axis > 2) raise(ST_INVAL, "axis must be 0, 1 or 2");
+    if (e->steps > 0)
+        raise(ST_INVAL, "the CPML profile can only be replaced before the first step");
+    const int n = e->gn[axis], nd = e->nd[axis];
+    if (a)
+        for (int g = nd; g < n - nd; ++g)
+            if (a[g] != 0.0f)
+                raise(ST_INVAL, "CPML coefficient a must be zero outside the damping layers");
+    if (a) std::memcpy(e->prof.a[axis].data(), a, n * sizeof(float));
+    if (b) std::memcpy(e->prof.b[axis].data(), b, n * sizeof(float));
+    if (inv_kappa) std::memcpy(e->prof.ik[axis].data(), inv_kappa, n * sizeof(float));
+    MM_CUDA(cudaStreamSynchronize(e->stream));
+    e->setup_cpml();
+    MM_CUDA(cudaStreamSynchronize(e->stream));
+    MM_API_END
+}
+
+int mm_cd_get_d0(mm_cd_engine* e, double d0[3]) {
+    MM_API_BEGIN
+    need(e, "engine");
+    need(d0, "d0");
+    for (int a = 0; a < 3; ++a) d0[a] = e->prof.d0[a];
+    MM_API_END
+}
+
+int mm_cd_set_receivers(mm_cd_engine* e, const int* ijk, int nreceivers, int capacity) {
+    MM_API_BEGIN
+    use(e);
+    if (nreceivers < 0 || capacity < 0) raise(ST_INVAL, "negative receiver count or capacity");
+    if (nreceivers > 0) need(ijk, "ijk");
+    std::vector<long long> offs(nreceivers);
+    for (int r = 0; r < nreceivers; ++r) {
+        const int* c = ijk + 3 * r;
+        for (int a = 0; a < 3; ++a)
+            if (c[a] < 0 || c[a] >= e->lay.n[a]) raise(ST_CONFIG, "receiver outside grid interior");
+        offs[r] = e->lay.off(c[0], c[1], c[2]);
+    }
+    e->rec_ijk.assign(ijk, ijk + 3 * (size_t)nreceivers);
+    e->nrec = nreceivers;
+    e->cap = capacity;
+    e->rec_offs.upload(offs.data(), offs.size(), e->stream);
+    e->traces.alloc_zero((size_t)nreceivers * capacity, e->stream);
+    MM_CUDA(cudaStreamSynchronize(e->stream));
+    MM_API_END
+}
+
+int mm_cd_record(mm_cd_engine* e, int step) {
+    MM_API_BEGIN
+    use(e);
+    if (step < 0 || step >= e->cap) raise(ST_INVAL, "record step outside the trace capacity");
+    RecParams rp{e->p[e->ic].ptr, e->rec_offs.ptr, e->traces.ptr, e->nrec, step, nullptr};
+    launch_record(rp, nullptr, e->stream);
+    MM_API_END
+}
+
+int mm_cd_get_traces(mm_cd_engine* e, float* host, int nsteps) {
+    MM_API_BEGIN
+    use(e);
+    need(host, "host");
+    if (nsteps < 0 || nsteps > e->cap) raise(ST_INVAL, "nsteps exceeds the trace capacity");
+    std::vector<float> dev((size_t)e->nrec * nsteps);
+    if (!dev.empty())
+        MM_CUDA(cudaMemcpyAsync(dev.data(), e->traces.ptr, dev.size() * sizeof(float),
+                                cudaMemcpyDeviceToHost, e->stream));
+    MM_CUDA(cudaStreamSynchronize(e->stream));
+    for (int s = 0; s < nsteps; ++s)
+        for (int r = 0; r < e->nrec; ++r)
+            host[(size_t)r * nsteps + s] = dev[(size_t)s * e->nrec + r];
+    MM_API_END
+}
+
+int mm_cd_copy_trace_step(mm_cd_engine* e, int step, float* host, int async) {
+    MM_API_BEGIN
+    use(e);
+    need(host, "host");
+    if (step < 0 || step >= e->cap) raise(ST_INVAL, "step outside the trace capacity");
+    if (e->nrec == 0) return MM_OK;
+    MM_CUDA(cudaMemcpyAsync(host, e->traces.ptr + (size_t)step * e->nrec,
+                            sizeof(float) * e->nrec, cudaMemcpyDeviceToHost, e->stream));
+    if (!async) MM_CUDA(cudaStreamSynchronize(e->stream));
+    MM_API_END
+}
+
+int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src, int record,
+              int first_sample, float* device_ms) {
+    MM_API_BEGIN
+    use(e);
+    if (nsteps < 0) raise(ST_INVAL, "nsteps must be >= 0");
+    if (nsteps == 0) return MM_OK;
+    need(amps, "amps");
+    if (record && (first_sample < 0 || first_sample + nsteps > e->cap))
+        raise(ST_INVAL, "recorded steps exceed the trace capacity");
+    if (src) (void)e->src_off(src);
+    e->amps.upload(amps, nsteps, e->stream);
+    const int init[2] = {0, INT_MAX};
+    MM_CUDA(cudaMemcpyAsync(e->counters.ptr, init, sizeof init, cudaMemcpyHostToDevice,
+                            e->stream));
+    int* step_dev = e->counters.ptr;
+    int* bad = e->counters.ptr + 1;
+    cudaEvent_t t0, t1;
+    MM_CUDA(cudaEventCreate(&t0));
+    MM_CUDA(cudaEventCreate(&t1));
+    MM_CUDA(cudaEventRecord(t0, e->stream));
+    for (int s = 0; s < nsteps; ++s) {
+        e->full_step(0.0f, src, e->amps.ptr, step_dev);
+        if (record && e->nrec > 0) {
+            RecParams rp{e->p[e->ic].ptr, e->rec_offs.ptr,
+                         e->traces.ptr + (size_t)first_sample * e->nrec, e->nrec, 0, bad};
+            launch_record(rp, step_dev, e->stream);
+        }
+        launch_step_counter(step_dev, e->stream);
+    }
+    MM_CUDA(cudaEventRecord(t1, e->stream));
+    MM_CUDA(cudaEventSynchronize(t1));
+    float ms = 0;
+    MM_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (device_ms) *device_ms = ms;
+    int bad_h = INT_MAX;
+    MM_CUDA(cudaMemcpy(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (bad_h != INT_MAX)
+        throw Error(ST_INSTABILITY,
+                    "non-finite wavefield sample detected at time step " +
+                        std::to_string(first_sample + bad_h),
+                    first_sample + bad_h);
+    MM_API_END
+}
+
+int mm_cd_stream(mm_cd_engine* e, void** stream) {
+    MM_API_BEGIN
+    need(e, "engine");
+    need(stream, "stream");
+    *stream = (void*)e->stream;
+    MM_API_END
+}
+
+static void halo_range(mm_cd_engine* e, int buf, int side, int which, void** ptr, size_t* bytes) {
+    need(ptr, "dev_ptr");
+    need(bytes, "bytes");
+    if (side < 0 || side > 1 || which < 0 || which > 1) raise(ST_INVAL, "side/which must be 0 or 1");
+    const Layout& L = e->lay;
+    const int nz = L.n[2], r = L.r;
+    if (nz < r) raise(ST_INVAL, "slab thinner than the stencil radius");
+    // plane index in [0, ez): ghost low [0,r), owned low [r,2r),
+    // owned high [nz, nz+r), ghost high [nz+r, nz+2r)
+    long long first;
+    if (side == 0)
+        first = which == 0 ? r : 0;
+    else
+        first = which == 0 ? nz : nz + r;
+    *ptr = (void*)(e->p[buf].ptr + first * L.plane);
+    *bytes = (size_t)r * L.plane * sizeof(float);
+}
+
+int mm_cd_halo_planes(mm_cd_engine* e, int side, int which, void** dev_ptr, size_t* bytes) {
+    MM_API_BEGIN
+    need(e, "engine");
+    halo_range(e, e->ic, side, which, dev_ptr, bytes);
+    MM_API_END
+}
+
+int mm_cd_next_halo_planes(mm_cd_engine* e, int side, int which, void** dev_ptr, size_t* bytes) {
+    MM_API_BEGIN
+    need(e, "engine");
+    halo_range(e, e->in, side, which, dev_ptr, bytes);
+    MM_API_END
+}
+
+int mm_sim_config_default(mm_sim_config* c) {
+    MM_API_BEGIN
+    need(c, "cfg");
+    std::memset(c, 0, sizeof *c);
+    for (int a = 0; a < 3; ++a) {
+        c->ngrid[a] = 100;
+        c->dgrid[a] = 20.0;
+        c->ndamping[a] = 27;
+        c->ntaper[a] = 3;
+    }
+    c->nsteps = 1000;
+    c->fmax = 25.0;
+    c->cfl = 0.8;
+    c->taper = 1;
+    c->free_surface = 0;
+    c->r_target = 1e-3;
+    c->has_source_loc = 0;
+    c->receiver_increment[0] = c->receiver_increment[1] = 1;
+    c->stencil_radius = 4;
+    MM_API_END
+}
+
+int mm_run(const mm_sim_config* c, const float* vp_model, int device, int mode, float* traces,
+           mm_run_report* rep) {
+    MM_API_BEGIN
+    need(c, "cfg");
+    need(vp_model, "vp_model");
+    const auto wall0 = std::chrono::steady_clock::now();
+    if (c->nsteps < 1) raise(ST_CONFIG, "nsteps must be >= 1");
+    for (int a = 0; a < 3; ++a) {
+        if (c->ngrid[a] < 1) raise(ST_CONFIG, "grid size must be >= 1");
+        if (!(c->dgrid[a] > 0.0)) raise(ST_CONFIG, "grid spacing must be > 0");
+    }
+    if (c->stencil_radius < 1) raise(ST_CONFIG, "stencil radius must be >= 1");
+    const HostGrid g{{c->ngrid[0], c->ngrid[1], c->ngrid[2]}, c->stencil_radius};
+    std::vector<float> vp(vp_model, vp_model + g.volume());
+    float vmin = 0, vmax = 0;
+    validate_vp(vp.data(), g, &vmin, &vmax);
+    fill_ghosts_replicate(vp.data(), g);
+    // driver.cpp:88-96
+    const double dt = cfl_dt(vmax, c->ngrid, c->dgrid, c->stencil_radius, c->cfl);
+    const std::vector<float> w = ricker(c->fmax, dt, c->nsteps);
+    int src[3] = {c->ngrid[0] / 2, c->ngrid[1] / 2, c->ngrid[2] / 2};
+    if (c->has_source_loc)
+        for (int a = 0; a < 3; ++a) src[a] = c->source_loc[a];
+    for (int a = 0; a < 3; ++a)
+        if (src[a] < 0 || src[a] >= c->ngrid[a])
+            raise(ST_CONFIG, "source location outside grid interior");
+    // default receiver carpet (source.cpp:40-50)
+    const int inc0 = c->receiver_increment[0], inc1 = c->receiver_increment[1];
+    if (inc0 < 1 || inc1 < 1) raise(ST_CONFIG, "receiver increment must be >= 1");
+    std::vector<int> rec;
+    for (int i = 0; i < c->ngrid[0]; i += inc0)
+        for (int j = 0; j < c->ngrid[1]; j += inc1) {
+            rec.push_back(i);
+            rec.push_back(j);
+            rec.push_back(c->ndamping[2]);
+        }
+    const int nrec = (int)rec.size() / 3;
+    mm_grid grid;
+    for (int a = 0; a < 3; ++a) {
+        grid.n[a] = c->ngrid[a];
+        grid.d[a] = c->dgrid[a];
+    }
+    grid.radius = c->stencil_radius;
+    mm_engine_options o;
+    for (int a = 0; a < 3; ++a) {
+        o.ndamping[a] = c->ndamping[a];
+        o.ntaper[a] = c->ntaper[a];
+    }
+    o.fmax = c->fmax;
+    o.r_target = c->r_target;
+    o.free_surface = c->free_surface;
+    o.taper = c->taper;
+    const int zero[3] = {0, 0, 0};
+    mm_cd_engine* e = nullptr;
+    int rc = mm_cd_create(&grid, zero, c->ngrid, vp.data(), &o, static_cast<float>(dt), vmax,
+                          device, mode, &e);
+    if (rc) return rc;
+    std::unique_ptr<mm_cd_engine, int (*)(mm_cd_engine*)> guard(e, mm_cd_destroy);
+    rc = mm_cd_set_receivers(e, rec.data(), nrec, c->nsteps);
+    if (rc) return rc;
+    float ms = 0;
+    rc = mm_cd_run(e, w.data(), c->nsteps, src, 1, 0, &ms);
+    if (rc) return rc;
+    if (traces) {
+        rc = mm_cd_get_traces(e, traces, c->nsteps);
+        if (rc) return rc;
+    }
+    // driver.cpp:120 check_finite(p(src), nsteps)
+    float ps = 0;
+    MM_CUDA(cudaMemcpy(&ps, e->p[e->ic].ptr + e->lay.off(src[0], src[1], src[2]), sizeof(float),
+                       cudaMemcpyDeviceToHost));
+    if (!std::isfinite(ps))
+        throw Error(ST_INSTABILITY,
+                    "non-finite wavefield sample detected at time step " +
+                        std::to_string(c->nsteps),
+                    c->nsteps);
+    if (rep) {
+        rep->dt = dt;
+        rep->kernel_seconds = ms * 1e-3;
+        rep->steps_run = c->nsteps;
+        rep->nreceivers = nrec;
+        rep->modeling_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    }
+    MM_API_END
+}
+
+}  // extern "C"

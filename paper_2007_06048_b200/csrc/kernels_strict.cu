@@ -1,0 +1,314 @@
+// kernels_strict.cu -- bit-exact (MM_MODE_STRICT) step kernels + plumbing kernels.
+//
+// One thread per grid point, reference association order, every operation an
+// explicitly rounded __fadd_rn/__fsub_rn/__fmul_rn (never contracted to FMA),
+// so results equal the CPU reference bit for bit:
+//   k_strict_update  = update_plain (propagator_impl.hpp:89-104, stencil.hpp:70-82)
+//                      + update_damping_pass2 (propagator_impl.hpp:125-152)
+//   k_strict_pass1   = update_damping_pass1 (propagator_impl.hpp:106-123)
+// The CPML memory lives in compact per-axis arrays over the active (a != 0)
+// layer indices; the per-slab zero-halo semantics of the reference's
+// BoxArray (cpml.hpp:77-99) are reproduced by the slab mask below (see
+// DESIGN.md "CPML masking rule").
+#include <climits>
+
+#include "mm_internal.hpp"
+
+namespace mmb {
+
+namespace {
+
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+
+// second_derivative_at (stencil.hpp:86-91): t += c_m * ((p[+m] + p[-m]) - 2 p0)
+template <int R>
+__device__ __forceinline__ float d2_strict(const float* q, long long s, const float* c,
+                                           float two_p0) {
+    float t = 0.0f;
+#pragma unroll
+    for (int m = 1; m <= R; ++m)
+        t = fadd(t, fmul(c[m - 1], fsub(fadd(__ldg(q + m * s), __ldg(q - m * s)), two_p0)));
+    return t;
+}
+
+__device__ __forceinline__ long long compact_off(const StepParams& p, int ax, int i, int j, int k,
+                                                 int ci) {
+    if (ax == 0) return ci + j * p.cs1[0] + k * p.cs2[0];
+    if (ax == 1) return i + ci * p.cs1[1] + k * p.cs2[1];
+    return i + j * p.cs1[2] + ci * p.cs2[2];
+}
+
+// psi_ax at local (i,j,k) shifted by `sh` along ax; zero outside the local
+// box or outside the active layer (the reference's zero halo).
+__device__ __forceinline__ float psi_at(const StepParams& p, int ax, int i, int j, int k, int sh) {
+    int loc[3] = {i, j, k};
+    loc[ax] += sh;
+    const int l = loc[ax];
+    if (l < 0 || l >= p.lay.n[ax]) return 0.0f;
+    const int ci = __ldg(p.map[ax] + l);
+    if (ci < 0) return 0.0f;
+    return __ldg(p.psi[ax] + compact_off(p, ax, loc[0], loc[1], loc[2], ci));
+}
+
+template <int R>
+__global__ void k_strict_update(StepParams p, int region, int z_lo) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = z_lo + blockIdx.z;
+    if (i >= p.lay.n[0] || j >= p.lay.n[1]) return;
+    const int g[3] = {i + p.goff[0], j + p.goff[1], k + p.goff[2]};
+    bool in[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) in[a] = g[a] >= p.nd[a] && g[a] < p.gn[a] - p.nd[a];
+    const bool inner = in[0] && in[1] && in[2];
+    if ((region == 1 && !inner) || (region == 2 && inner)) return;
+
+    const long long o = p.lay.off(i, j, k);
+    const float* q = p.pc + o;
+    const long long s[3] = {1, p.lay.P, p.lay.plane};
+    const float two_p0 = fmul(2.0f, q[0]);
+    float lap;
+    if (inner) {
+        const float tx = d2_strict<R>(q, s[0], p.c2[0], two_p0);
+        const float ty = d2_strict<R>(q, s[1], p.c2[1], two_p0);
+        const float tz = d2_strict<R>(q, s[2], p.c2[2], two_p0);
+        lap = fadd(fadd(tx, ty), tz);
+    } else {
+        // slab membership (grid.cpp:34-41): X slabs span all y,z; Y slabs the
+        // inner x range; Z slabs the inner x,y range.  dpsi_ax reads psi only
+        // inside the point's own slab box, which is what these masks encode.
+        const bool use[3] = {!in[0], !in[0] || !in[1], true};
+        const int loc[3] = {i, j, k};
+        float term[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const float d2p = d2_strict<R>(q, s[ax], p.c2[ax], two_p0);
+            const int l = loc[ax];
+            const float a = __ldg(p.ta[ax] + l), b = __ldg(p.tb[ax] + l),
+                        ik = __ldg(p.tik[ax] + l);
+            float dpsi = 0.0f;
+            if (use[ax]) {
+#pragma unroll
+                for (int m = 1; m <= R; ++m)
+                    dpsi = fadd(dpsi, fmul(p.c1[ax][m - 1], fsub(psi_at(p, ax, i, j, k, m),
+                                                                 psi_at(p, ax, i, j, k, -m))));
+            }
+            const float drive = fadd(fmul(d2p, ik), dpsi);
+            const int ci = __ldg(p.map[ax] + l);
+            float z;
+            if (ci >= 0) {
+                float* zp = p.zeta[ax] + compact_off(p, ax, i, j, k, ci);
+                z = fadd(fmul(b, *zp), fmul(a, drive));
+                *zp = z;
+            } else {
+                z = fadd(fmul(b, 0.0f), fmul(a, drive));
+            }
+            term[ax] = fadd(drive, z);
+        }
+        lap = fadd(fadd(term[0], term[1]), term[2]);
+    }
+    p.pn[o] = fadd(fsub(two_p0, p.pp[o]), fmul(p.cv[o], lap));
+}
+
+// Pass 1 over the compact storage of one axis: psi = b psi + a D1(p_cur).
+template <int R>
+__global__ void k_strict_pass1(StepParams p, int ax, int ext0, int ext1, int ext2, int z_lo,
+                               int z_hi) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int z = blockIdx.z;
+    if (x >= ext0 || y >= ext1 || z >= ext2) return;
+    int loc[3] = {x, y, z};
+    loc[ax] = __ldg(p.list[ax] + loc[ax]);
+    if (loc[2] < z_lo || loc[2] >= z_hi) return;
+    const long long s[3] = {1, p.lay.P, p.lay.plane};
+    const float* q = p.pc + p.lay.off(loc[0], loc[1], loc[2]);
+    float dp = 0.0f;
+#pragma unroll
+    for (int m = 1; m <= R; ++m)
+        dp = fadd(dp, fmul(p.c1[ax][m - 1], fsub(__ldg(q + m * s[ax]), __ldg(q - m * s[ax]))));
+    const int l = loc[ax];
+    const float a = __ldg(p.ta[ax] + l), b = __ldg(p.tb[ax] + l);
+    const int ci = ax == 0 ? x : ax == 1 ? y : z;
+    float* ps = p.psi[ax] + compact_off(p, ax, loc[0], loc[1], loc[2], ci);
+    *ps = fadd(fmul(b, *ps), fmul(a, dp));
+}
+
+template <int R>
+void strict_pass1_r(const StepParams& p, int z_lo, int z_hi, cudaStream_t st) {
+    for (int ax = 0; ax < 3; ++ax) {
+        if (p.cnt[ax] == 0) continue;
+        int ext[3] = {p.lay.n[0], p.lay.n[1], p.lay.n[2]};
+        ext[ax] = p.cnt[ax];
+        dim3 blk(32, 8, 1);
+        dim3 grd((ext[0] + 31) / 32, (ext[1] + 7) / 8, ext[2]);
+        k_strict_pass1<R><<<grd, blk, 0, st>>>(p, ax, ext[0], ext[1], ext[2], z_lo, z_hi);
+        note_launches(1);
+    }
+}
+
+template <int R>
+void strict_update_r(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t st) {
+    if (z_hi <= z_lo) return;
+    dim3 blk(32, 8, 1);
+    dim3 grd((p.lay.n[0] + 31) / 32, (p.lay.n[1] + 7) / 8, z_hi - z_lo);
+    k_strict_update<R><<<grd, blk, 0, st>>>(p, region, z_lo);
+    note_launches(1);
+}
+
+__global__ void k_inject(float* pn, const float* cv, long long off, float amp,
+                         const float* amp_dev, const int* step_dev) {
+    // ref: propagator_impl.hpp:166-169  p_next[src] += ((dt2 vp) vp) amp
+    const float a = amp_dev ? amp_dev[*step_dev] : amp;
+    pn[off] = __fadd_rn(pn[off], __fmul_rn(cv[off], a));
+}
+
+__global__ void k_free_surface(float* p, Layout lay) {
+    // ref: cpml.hpp:103-111, over i,j in [-r, n+r)
+    const int i = blockIdx.x * blockDim.x + threadIdx.x - lay.r;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y - lay.r;
+    if (i >= lay.n[0] + lay.r || j >= lay.n[1] + lay.r) return;
+    p[lay.off(i, j, 0)] = 0.0f;
+    for (int m = 1; m <= lay.r; ++m) p[lay.off(i, j, -m)] = -p[lay.off(i, j, m)];
+}
+
+__global__ void k_record(RecParams rp, const int* step_dev) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rp.nrec) return;
+    const int step = step_dev ? *step_dev : rp.step;
+    const float v = rp.p[rp.offs[r]];
+    rp.traces[(long long)step * rp.nrec + r] = v;
+    // ref: driver.cpp:68-71,108 check_finite(rec.at(0, n), n + 1)
+    if (r == 0 && !isfinite(v) && rp.bad_step) atomicMin(rp.bad_step, step + 1);
+}
+
+__global__ void k_step_counter(int* step_dev) { *step_dev += 1; }
+
+// Host layout (i slowest, k fastest, ghosted) <-> device layout (k slowest,
+// i fastest, ghosted + padded), tiled 32x32 transposes over (i, k) per j.
+__global__ void k_to_device(const float* __restrict__ h, float* __restrict__ d, Layout lay) {
+    __shared__ float tile[32][33];
+    const int ex = lay.n[0] + 2 * lay.r, ey = lay.ey, ez = lay.ez;
+    const int j = blockIdx.z;
+    const int k0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    for (int t = threadIdx.y; t < 32; t += blockDim.y) {
+        const int i = i0 + t, k = k0 + threadIdx.x;
+        if (i < ex && k < ez) tile[t][threadIdx.x] = h[((long long)i * ey + j) * ez + k];
+    }
+    __syncthreads();
+    for (int t = threadIdx.y; t < 32; t += blockDim.y) {
+        const int k = k0 + t, i = i0 + threadIdx.x;
+        if (i < ex && k < ez)
+            d[((long long)k * ey + j) * lay.P + (i - lay.r + lay.L)] = tile[threadIdx.x][t];
+    }
+}
+
+__global__ void k_to_host(const float* __restrict__ d, float* __restrict__ h, Layout lay) {
+    __shared__ float tile[32][33];
+    const int ex = lay.n[0] + 2 * lay.r, ey = lay.ey, ez = lay.ez;
+    const int j = blockIdx.z;
+    const int k0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    for (int t = threadIdx.y; t < 32; t += blockDim.y) {
+        const int k = k0 + t, i = i0 + threadIdx.x;
+        if (i < ex && k < ez)
+            tile[t][threadIdx.x] = d[((long long)k * ey + j) * lay.P + (i - lay.r + lay.L)];
+    }
+    __syncthreads();
+    for (int t = threadIdx.y; t < 32; t += blockDim.y) {
+        const int i = i0 + t, k = k0 + threadIdx.x;
+        if (i < ex && k < ez) h[((long long)i * ey + j) * ez + k] = tile[threadIdx.x][t];
+    }
+}
+
+__global__ void k_velocity_coeff(const float* vp, float* cv, float dt2, long long total) {
+    // (dt2 * vp) * vp: bit-identical to the reference's dt2_*vp*vp
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x)
+        cv[x] = __fmul_rn(__fmul_rn(dt2, vp[x]), vp[x]);
+}
+
+}  // namespace
+
+#define MM_RADIUS_SWITCH(R_, CALL)                                   \
+    switch (R_) {                                                    \
+        case 1: CALL(1); break;                                      \
+        case 2: CALL(2); break;                                      \
+        case 3: CALL(3); break;                                      \
+        case 4: CALL(4); break;                                      \
+        case 5: CALL(5); break;                                      \
+        case 6: CALL(6); break;                                      \
+        case 7: CALL(7); break;                                      \
+        case 8: CALL(8); break;                                      \
+        default: raise(ST_CONFIG, "stencil radius must be in [1, 8]"); \
+    }
+
+void strict_pass1(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) {
+#define CALL(R) strict_pass1_r<R>(p, z_lo, z_hi, s)
+    MM_RADIUS_SWITCH(p.lay.r, CALL)
+#undef CALL
+    MM_CUDA(cudaGetLastError());
+}
+
+void strict_update(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t s) {
+#define CALL(R) strict_update_r<R>(p, region, z_lo, z_hi, s)
+    MM_RADIUS_SWITCH(p.lay.r, CALL)
+#undef CALL
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_inject(float* pn, const float* cv, long long off, float amp, const float* amp_dev,
+                   const int* step_dev, cudaStream_t s) {
+    k_inject<<<1, 1, 0, s>>>(pn, cv, off, amp, amp_dev, step_dev);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_free_surface(float* p, const Layout& lay, cudaStream_t s) {
+    dim3 blk(32, 8);
+    dim3 grd((lay.n[0] + 2 * lay.r + 31) / 32, (lay.n[1] + 2 * lay.r + 7) / 8);
+    k_free_surface<<<grd, blk, 0, s>>>(p, lay);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_record(const RecParams& rp, const int* step_dev, cudaStream_t s) {
+    if (rp.nrec == 0) return;
+    k_record<<<(rp.nrec + 255) / 256, 256, 0, s>>>(rp, step_dev);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_step_counter(int* step_dev, cudaStream_t s) {
+    k_step_counter<<<1, 1, 0, s>>>(step_dev);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_to_device_layout(const float* h, float* d, const Layout& lay, cudaStream_t s) {
+    const int ex = lay.n[0] + 2 * lay.r;
+    dim3 blk(32, 8);
+    dim3 grd((lay.ez + 31) / 32, (ex + 31) / 32, lay.ey);
+    k_to_device<<<grd, blk, 0, s>>>(h, d, lay);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_to_host_layout(const float* d, float* h, const Layout& lay, cudaStream_t s) {
+    const int ex = lay.n[0] + 2 * lay.r;
+    dim3 blk(32, 8);
+    dim3 grd((lay.ez + 31) / 32, (ex + 31) / 32, lay.ey);
+    k_to_host<<<grd, blk, 0, s>>>(d, h, lay);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_velocity_coeff(const float* vp, float* cv, float dt2, long long total,
+                           cudaStream_t s) {
+    k_velocity_coeff<<<1184, 256, 0, s>>>(vp, cv, dt2, total);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+}  // namespace mmb

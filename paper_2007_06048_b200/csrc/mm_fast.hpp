@@ -1,0 +1,26 @@
+// mm_fast.hpp -- the MM_MODE_FAST step (TMA-fed 2.5D kernels), see kernels_fast.cu.
+#pragma once
+
+#include <memory>
+
+#include "mm_internal.hpp"
+
+namespace mmb {
+
+class FastPlan {
+public:
+    virtual ~FastPlan() = default;
+    // CPML pass 1 over the compact psi storage (all local planes).
+    virtual void pass1(const StepParams& p, cudaStream_t s) = 0;
+    // Pass 2 + inner update on local planes [z_lo, z_hi); region as strict_update.
+    virtual void update(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t s) = 0;
+    // One whole step (pass 1, update, source injection); src_off < 0: no source.
+    virtual void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
+                      const int* step_dev, cudaStream_t s) = 0;
+};
+
+// nullptr when the fast kernels cannot serve this layout (the engine then
+// runs the strict kernels, which are exact for every radius).
+std::unique_ptr<FastPlan> make_fast_plan(const Layout& lay, int device);
+
+}  // namespace mmb

@@ -1,0 +1,138 @@
+// mm_internal.hpp -- shared internals of the B200 acoustic_iso_cd library.
+//
+// Device layout: x fastest, z slowest,
+// the reverse of the reference's z-fastest host layout (grid.hpp:61-65), so
+// that z-slabs, halo planes and the receiver plane are contiguous and the
+// 2.5D kernels stream along the slowest axis.
+//   dev_off(i,j,k) = ((k + r) * ey + (j + r)) * P + (i + L)
+//   L = round_up(r, 4)     left x pad: interior x = 0 is 16-byte aligned
+//   P = round_up(L + nx + r, 32)   row pitch (128-byte rows)
+//   ey = ny + 2r, ez = nz + 2r
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace mmb {
+
+// ---------------------------------------------------------------- errors
+enum Status { ST_OK = 0, ST_CONFIG = 1, ST_VALIDATION = 2, ST_INSTABILITY = 3, ST_INVAL = 4, ST_CUDA = 5,
+              ST_NCCL = 6 };
+
+struct Error : std::runtime_error {
+    int code;
+    int step;
+    Error(int c, const std::string& m, int s = 0) : std::runtime_error(m), code(c), step(s) {}
+};
+
+[[noreturn]] inline void raise(int code, const std::string& msg) { throw Error(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define MM_CUDA(x) ::mmb::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Counts kernel launches issued through the library (evidence for bench.py).
+void note_launches(long long n);
+
+// ---------------------------------------------------------------- numerics
+// All of these restate the reference bit for bit (see host_numerics.cpp).
+struct Coeffs {
+    std::vector<double> c;  // taps m = 1..radius (c[m-1])
+    double center = 0.0;
+};
+Coeffs second_derivative(int radius, double h);      // ref: stencil.cpp:50-74
+Coeffs central_first_derivative(int radius, double h);  // ref: stencil.cpp:99-117
+double cfl_dt(double vmax, const int n[3], const double d[3], int radius, double cfl);
+std::vector<float> ricker(double fmax, double dt, int nsteps);
+
+struct Profile {  // ref: cpml.hpp:13-26 (float tables over the global axis)
+    std::vector<float> a[3], b[3], ik[3];
+    double d0[3] = {0, 0, 0};
+};
+Profile build_profile(const int n[3], const double h[3], const int nd[3], double fmax,
+                      double vmax, double dt, double r_target, bool free_surface);
+
+// Host reference-layout helpers (ghosted, z fastest).
+struct HostGrid {
+    int n[3];
+    int r;
+    size_t ext(int a) const { return (size_t)n[a] + 2 * r; }
+    size_t volume() const { return ext(0) * ext(1) * ext(2); }
+    size_t off(int i, int j, int k) const {
+        return ((size_t)(i + r) * ext(1) + (size_t)(j + r)) * ext(2) + (size_t)(k + r);
+    }
+};
+void fill_ghosts_replicate(float* f, const HostGrid& g);
+void taper_material(float* f, const HostGrid& g, const int ntaper[3], const int offset[3],
+                    const int global_n[3]);
+void validate_vp(const float* vp, const HostGrid& g, float* vmin, float* vmax);
+
+// ---------------------------------------------------------------- device
+struct Layout {
+    int n[3];
+    int r, L, P, ey, ez;
+    long long plane;  // ey * P
+    long long total;  // plane * ez
+    static Layout make(const int n[3], int r);
+    __host__ __device__ long long off(int i, int j, int k) const {
+        return ((long long)(k + r) * ey + (j + r)) * (long long)P + (i + L);
+    }
+};
+
+constexpr int kMaxR = 8;
+
+// Everything a step kernel needs, passed by value.
+struct StepParams {
+    Layout lay;
+    int goff[3];  // local -> global index offset
+    int gn[3];    // global interior size
+    int nd[3];    // ndamping (region partition, grid.cpp:24-45)
+    const float* pc;  // p_cur
+    const float* pp;  // p_prev
+    float* pn;        // p_next
+    const float* cv;  // (dt2 * vp) * vp, device layout
+    float c2[3][kMaxR];  // second-derivative taps per axis (float, 1/h^2 folded)
+    float c1[3][kMaxR];  // central first-derivative taps per axis
+    // CPML: local tables (length n[ax]), active-index maps and compact storage
+    const float* ta[3];
+    const float* tb[3];
+    const float* tik[3];
+    const int* map[3];   // local index -> compact index, -1 if inactive (a == 0)
+    const int* list[3];  // compact index -> local index
+    int cnt[3];          // number of active indices per axis
+    float* psi[3];
+    float* zeta[3];
+    long long cs1[3], cs2[3];  // compact strides of y and z per axis (x stride 1)
+};
+
+// Receiver sampling, device trace layout [step][receiver].
+struct RecParams {
+    const float* p;
+    const long long* offs;  // device offsets of receivers
+    float* traces;
+    int nrec;
+    int step;
+    int* bad_step;  // first 1-based step with non-finite receiver 0 (INT_MAX if none)
+};
+
+// ---- launchers (kernels_strict.cu)
+void strict_pass1(const StepParams& p, int z_lo, int z_hi, cudaStream_t s);
+// region: 0 = every point, 1 = inner box only, 2 = damping slabs only
+void strict_update(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t s);
+void launch_inject(float* pn, const float* cv, long long off, float amp, const float* amp_dev,
+                   const int* step_dev, cudaStream_t s);
+void launch_free_surface(float* p, const Layout& lay, cudaStream_t s);
+void launch_record(const RecParams& rp, const int* step_dev, cudaStream_t s);
+void launch_step_counter(int* step_dev, cudaStream_t s);
+void launch_to_device_layout(const float* host_layout, float* dev_layout, const Layout& lay,
+                             cudaStream_t s);
+void launch_to_host_layout(const float* dev_layout, float* host_layout, const Layout& lay,
+                           cudaStream_t s);
+void launch_velocity_coeff(const float* vp_dev_layout, float* cv, float dt2, long long total,
+                           cudaStream_t s);
+
+}  // namespace mmb

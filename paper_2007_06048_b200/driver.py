@@ -1,0 +1,106 @@
+"""run() -- the reference's modeling driver on the GPU (acoustic_iso_cd only).
+
+ref: driver.hpp:21-54 (SimConfig, RunReport), driver.cpp:19-29 (cfl_dt),
+driver.cpp:37-47 (build_geometry), driver.cpp:83-144 (run).  The time loop
+itself runs in C++ (``mm_run`` in csrc/engine.cu): device-resident wavelet,
+device receiver recording, one receiver-0 finiteness check per step.
+``kernel_seconds`` is the device time of the step loop (CUDA events), the
+analogue of the reference's "Time Kernel" (driver.cpp:102-107).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import ConfigError, check, lib
+from .numerics import (AcquisitionGeometry, EarthModel, Grid3D, ShotRecord, default_receivers,
+                       make_grid)
+
+
+@dataclass
+class SimConfig:  # ref: driver.hpp:21-47 (acoustic_iso_cd subset, same defaults)
+    ngrid: tuple = (100, 100, 100)
+    dgrid: tuple = (20.0, 20.0, 20.0)
+    nsteps: int = 1000
+    fmax: float = 25.0
+    cfl: float = 0.8
+    ndamping: tuple = (27, 27, 27)
+    ntaper: tuple = (3, 3, 3)
+    taper: bool = True
+    free_surface: bool = False
+    r_target: float = 1e-3
+    source_loc: Optional[tuple] = None
+    receiver_increment: tuple = (1, 1)
+    stencil_radius: int = 4
+
+    def to_c(self) -> _lib.mm_sim_config:
+        c = _lib.mm_sim_config()
+        check(lib().mm_sim_config_default(C.byref(c)))
+        c.ngrid[:] = [int(x) for x in self.ngrid]
+        c.dgrid[:] = [float(x) for x in self.dgrid]
+        c.nsteps = int(self.nsteps)
+        c.fmax = float(self.fmax)
+        c.cfl = float(self.cfl)
+        c.ndamping[:] = [int(x) for x in self.ndamping]
+        c.ntaper[:] = [int(x) for x in self.ntaper]
+        c.taper = int(bool(self.taper))
+        c.free_surface = int(bool(self.free_surface))
+        c.r_target = float(self.r_target)
+        c.has_source_loc = int(self.source_loc is not None)
+        if self.source_loc is not None:
+            c.source_loc[:] = [int(x) for x in self.source_loc]
+        c.receiver_increment[:] = [int(x) for x in self.receiver_increment]
+        c.stencil_radius = int(self.stencil_radius)
+        return c
+
+
+@dataclass
+class RunReport:  # ref: driver.hpp:49-54
+    dt: float = 0.0
+    kernel_seconds: float = 0.0
+    modeling_seconds: float = 0.0
+    steps_run: int = 0
+
+
+def cfl_dt(model: EarthModel, grid: Grid3D, cfl: float) -> float:  # ref: driver.cpp:19-29
+    g = _lib.mm_grid()
+    g.n[:] = list(grid.n)
+    g.d[:] = list(grid.d)
+    g.radius = grid.radius
+    dt = C.c_double()
+    check(lib().mm_cfl_dt(float(model.vmax), C.byref(g), float(cfl), C.byref(dt)))
+    return dt.value
+
+
+def build_geometry(config: SimConfig, grid: Grid3D) -> AcquisitionGeometry:
+    """ref: driver.cpp:37-47."""
+    g = default_receivers(grid, config.ndamping, config.receiver_increment)
+    if config.source_loc is not None:
+        g.source_loc = tuple(config.source_loc)
+    if not grid.interior().contains(*g.source_loc):
+        raise ConfigError("source location outside grid interior")
+    return g
+
+
+def run(config: SimConfig, model: EarthModel, *, device: int = 0,
+        mode: str = "fast") -> Tuple[ShotRecord, RunReport]:
+    """ref: driver.cpp:83-144 for acoustic_iso_cd."""
+    if tuple(model.grid.n) != tuple(config.ngrid):
+        raise ConfigError("model grid does not match configured ngrid")
+    grid = make_grid(config.ngrid, config.dgrid, config.stencil_radius)
+    geom = build_geometry(config, grid)
+    vp = np.ascontiguousarray(model.vp, dtype=np.float32)
+    if vp.shape != grid.shape:
+        raise ConfigError("model radius does not match the stencil radius")
+    traces = np.zeros((geom.nreceivers(), config.nsteps), np.float32)
+    rep = _lib.mm_run_report()
+    from .propagator import _MODES
+    check(lib().mm_run(C.byref(config.to_c()), vp.ctypes.data_as(C.POINTER(C.c_float)),
+                       int(device), _MODES[mode],
+                       traces.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rep)))
+    record = ShotRecord(config.nsteps, rep.dt, geom, traces)
+    return record, RunReport(rep.dt, rep.kernel_seconds, rep.modeling_seconds, rep.steps_run)

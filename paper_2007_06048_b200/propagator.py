@@ -1,0 +1,244 @@
+"""AcousticCdEngine -- Python mirror of minimod::AcousticCdEngine<float>.
+
+ref: propagator.hpp:93-140 (interface), propagator_impl.hpp:53-173
+(implementation).  Every call goes through the C ABI
+(include/minimod_b200.h) into the CUDA library; there is no CPU path.
+
+Differences from the C++ reference that callers may notice:
+* ``pressure()`` / ``pressure_prev()`` return host copies (the fields live in
+  HBM); write back with ``set_state``.
+* ``profile()`` returns a copy of the CPML tables; apply edits with
+  ``set_profile`` (accepted before the first step, as the reference tests
+  use it: test_cpml.cpp:148-153).
+* ``runner`` arguments are accepted and ignored (the GPU is the runner).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import MM_MODE_FAST, MM_MODE_STRICT, check, lib
+from .numerics import AxisCpml, CpmlProfile, Grid3D, make_grid
+
+_i3 = C.c_int * 3
+
+
+def _fptr(a: np.ndarray):
+    assert a.dtype == np.float32 and a.flags.c_contiguous
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+@dataclass
+class EngineOptions:  # ref: propagator.hpp:23-30 (same defaults)
+    ndamping: tuple = (0, 0, 0)
+    fmax: float = 25.0
+    r_target: float = 1e-3
+    free_surface: bool = False
+    taper: bool = False
+    ntaper: tuple = (3, 3, 3)
+
+    def to_c(self) -> _lib.mm_engine_options:
+        o = _lib.mm_engine_options()
+        o.ndamping[:] = [int(x) for x in self.ndamping]
+        o.fmax = float(self.fmax)
+        o.r_target = float(self.r_target)
+        o.free_surface = int(bool(self.free_surface))
+        o.taper = int(bool(self.taper))
+        o.ntaper[:] = [int(x) for x in self.ntaper]
+        return o
+
+
+_MODES = {"fast": MM_MODE_FAST, "strict": MM_MODE_STRICT}
+
+
+class AcousticCdEngine:
+    """Second-order constant-density acoustic propagator with CPML on the GPU."""
+
+    def __init__(self, grid: Grid3D, offset: Sequence[int], global_n: Sequence[int],
+                 vp_local: np.ndarray, opts: Optional[EngineOptions] = None,
+                 dt: float = 1e-3, vmax_global: Optional[float] = None, *, device: int = 0,
+                 mode: str = "fast"):
+        opts = opts or EngineOptions()
+        self._h = None
+        self._grid = grid
+        self.offset = tuple(int(x) for x in offset)
+        self.global_n = tuple(int(x) for x in global_n)
+        vp = np.ascontiguousarray(vp_local, dtype=np.float32)
+        if vp.shape != grid.shape:
+            raise ValueError(f"vp_local shape {vp.shape} != ghosted grid shape {grid.shape}")
+        if vmax_global is None:
+            vmax_global = float(grid.inner(vp).max())
+        g = _lib.mm_grid()
+        g.n[:] = list(grid.n)
+        g.d[:] = list(grid.d)
+        g.radius = grid.radius
+        h = C.c_void_p()
+        self.mode = mode
+        check(lib().mm_cd_create(C.byref(g), _i3(*self.offset), _i3(*self.global_n), _fptr(vp),
+                                 C.byref(opts.to_c()), C.c_float(dt), float(vmax_global),
+                                 int(device), _MODES[mode], C.byref(h)))
+        self._h = h
+        self.device = device
+        self.options = opts
+        self._nrec = 0
+        self._cap = 0
+
+    # -- lifetime ---------------------------------------------------------
+    def close(self):
+        if self._h:
+            lib().mm_cd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- reference interface ---------------------------------------------
+    def step(self, source_amplitude: float, src: Optional[Sequence[int]] = None, runner=None):
+        """ref: propagator.hpp:103-104."""
+        check(lib().mm_cd_step(self._h, C.c_float(source_amplitude),
+                               _i3(*src) if src is not None else None))
+
+    def grid(self) -> Grid3D:
+        return self._grid
+
+    def dt(self) -> float:
+        v = C.c_float()
+        check(lib().mm_cd_get_dt(self._h, C.byref(v)))
+        return v.value
+
+    def pressure(self) -> np.ndarray:
+        out = self._grid.field()
+        check(lib().mm_cd_get_pressure(self._h, _fptr(out)))
+        return out
+
+    def pressure_prev(self) -> np.ndarray:
+        out = self._grid.field()
+        check(lib().mm_cd_get_pressure_prev(self._h, _fptr(out)))
+        return out
+
+    def velocity(self) -> np.ndarray:
+        """The (tapered) vp copy the engine steps with."""
+        out = self._grid.field()
+        check(lib().mm_cd_get_velocity(self._h, _fptr(out)))
+        return out
+
+    def set_state(self, p_prev: np.ndarray, p_cur: np.ndarray):
+        """ref: propagator.hpp:116-120."""
+        a = np.ascontiguousarray(p_prev, dtype=np.float32)
+        b = np.ascontiguousarray(p_cur, dtype=np.float32)
+        if a.shape != self._grid.shape or b.shape != self._grid.shape:
+            raise ValueError("set_state fields must have the ghosted grid shape")
+        check(lib().mm_cd_set_state(self._h, _fptr(a), _fptr(b)))
+
+    def profile(self) -> CpmlProfile:
+        """Copy of the CPML tables (ref: propagator.hpp:112-114)."""
+        axes = []
+        for ax in range(3):
+            n = self.global_n[ax]
+            a, b, k = (np.zeros(n, np.float32) for _ in range(3))
+            check(lib().mm_cd_get_profile(self._h, ax, _fptr(a), _fptr(b), _fptr(k)))
+            axes.append(AxisCpml(a, b, k))
+        d0 = (C.c_double * 3)()
+        check(lib().mm_cd_get_d0(self._h, d0))
+        return CpmlProfile(axes, tuple(self.options.ndamping), tuple(d0))
+
+    def set_profile(self, prof: CpmlProfile):
+        for ax in range(3):
+            A = prof.axis[ax]
+            a = np.ascontiguousarray(A.a, np.float32)
+            b = np.ascontiguousarray(A.b, np.float32)
+            k = np.ascontiguousarray(A.inv_kappa, np.float32)
+            check(lib().mm_cd_set_profile(self._h, ax, _fptr(a), _fptr(b), _fptr(k)))
+
+    # -- sub-phases (ref: propagator_impl.hpp:154-173) --------------------
+    def update_boundary_psi(self):
+        check(lib().mm_cd_update_boundary_psi(self._h))
+
+    def update_inner(self):
+        check(lib().mm_cd_update_inner(self._h))
+
+    def update_boundary(self):
+        check(lib().mm_cd_update_boundary(self._h))
+
+    def update_planes(self, z_lo: int, z_hi: int):
+        check(lib().mm_cd_update_planes(self._h, int(z_lo), int(z_hi)))
+
+    def inject_source(self, amp: float, src: Optional[Sequence[int]]):
+        check(lib().mm_cd_inject_source(self._h, C.c_float(amp),
+                                        _i3(*src) if src is not None else None))
+
+    def apply_free_surface(self):
+        check(lib().mm_cd_apply_free_surface(self._h))
+
+    def rotate(self):
+        check(lib().mm_cd_rotate(self._h))
+
+    def synchronize(self):
+        check(lib().mm_cd_synchronize(self._h))
+
+    def steps_taken(self) -> int:
+        v = C.c_longlong()
+        check(lib().mm_cd_steps_taken(self._h, C.byref(v)))
+        return v.value
+
+    # -- receivers / device loop -----------------------------------------
+    def set_receivers(self, ijk: np.ndarray, capacity: int):
+        ijk = np.ascontiguousarray(ijk, dtype=np.int32).reshape(-1, 3)
+        check(lib().mm_cd_set_receivers(self._h, ijk.ctypes.data_as(C.POINTER(C.c_int)),
+                                        ijk.shape[0], int(capacity)))
+        self._nrec, self._cap = ijk.shape[0], int(capacity)
+
+    def record(self, step: int):
+        check(lib().mm_cd_record(self._h, int(step)))
+
+    def traces(self, nsteps: Optional[int] = None) -> np.ndarray:
+        nsteps = self._cap if nsteps is None else nsteps
+        out = np.zeros((self._nrec, nsteps), np.float32)
+        check(lib().mm_cd_get_traces(self._h, _fptr(out), int(nsteps)))
+        return out
+
+    def copy_trace_step(self, step: int, out: np.ndarray, asynchronous: bool = False):
+        """Receiver samples of one recorded step into `out` (nreceivers float32)."""
+        assert out.dtype == np.float32 and out.size >= self._nrec
+        check(lib().mm_cd_copy_trace_step(self._h, int(step), _fptr(out), int(asynchronous)))
+
+    def run(self, amps: np.ndarray, src: Optional[Sequence[int]] = None, record: bool = True,
+            first_sample: int = 0) -> float:
+        """Device-resident loop over len(amps) steps; returns device milliseconds."""
+        amps = np.ascontiguousarray(amps, dtype=np.float32)
+        ms = C.c_float()
+        check(lib().mm_cd_run(self._h, _fptr(amps), amps.size,
+                              _i3(*src) if src is not None else None, int(record),
+                              int(first_sample), C.byref(ms)))
+        return ms.value
+
+    # -- multi-GPU plumbing ----------------------------------------------
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        check(lib().mm_cd_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def halo_planes(self, side: int, which: int, next_field: bool = False):
+        """(device pointer, bytes) of the r contiguous z-planes (see the C ABI)."""
+        p = C.c_void_p()
+        n = C.c_size_t()
+        fn = lib().mm_cd_next_halo_planes if next_field else lib().mm_cd_halo_planes
+        check(fn(self._h, int(side), int(which), C.byref(p), C.byref(n)))
+        return p.value, n.value

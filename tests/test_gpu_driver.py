@@ -1,0 +1,89 @@
+"""GPU parity of the driver path run() (ref: driver.cpp:83-144) against the
+reference's golden traces and checksums, plus the device-loop contract."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_run_layered_32_golden(mm, mode):
+    g = load_golden("run_layered_32")
+    n = tuple(int(x) for x in g["n"])
+    cfg = mm.SimConfig(ngrid=n, nsteps=int(g["nsteps"]), ndamping=tuple(g["ndamping"]),
+                       ntaper=tuple(g["ntaper"]))
+    model = mm.default_layered_model(mm.make_grid(n, cfg.dgrid))
+    rec, rep = mm.run(cfg, model, mode=mode)
+    assert rep.dt == float(g["dt"]) and rep.steps_run == cfg.nsteps
+    assert rep.kernel_seconds > 0 and rep.kernel_seconds <= rep.modeling_seconds
+    if mode == "strict":
+        assert np.array_equal(rec.traces, g["traces"])
+    else:
+        assert rel_l2(rec.traces, g["traces"]) <= 1e-5
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_run_oracle_config_100(mm, mode):
+    """C1: 100^3 x 100 steps, layered, nd 27, taper on (BASELINE configs[0])."""
+    g = load_golden("run_layered_100")
+    cfg = mm.SimConfig(ngrid=(100, 100, 100), nsteps=100)
+    model = mm.default_layered_model(mm.make_grid(cfg.ngrid, cfg.dgrid))
+    rec, rep = mm.run(cfg, model, mode=mode)
+    got = rec.traces[g["pick"]]
+    if mode == "strict":
+        assert np.array_equal(got, g["traces"])
+        assert abs(np.linalg.norm(rec.traces.astype(np.float64)) - g["trace_norm"]) == 0
+    else:
+        assert rel_l2(got, g["traces"]) <= 1e-5
+        assert abs(np.linalg.norm(rec.traces.astype(np.float64)) / g["trace_norm"] - 1) < 1e-5
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_final_field_checksums_100(mm, mode):
+    """Final p_cur of C1 against the reference checksums."""
+    g = load_golden("run_layered_100")
+    grid = mm.make_grid((100, 100, 100), (20.0, 20.0, 20.0))
+    model = mm.default_layered_model(grid)
+    dt = mm.cfl_dt(model, grid, 0.8)
+    w = mm.ricker(25.0, dt, 100).samples
+    e = mm.AcousticCdEngine(grid, (0, 0, 0), grid.n, model.vp,
+                            mm.EngineOptions(ndamping=(27, 27, 27), taper=True), dt, model.vmax,
+                            mode=mode)
+    e.set_receivers(np.array([[0, 0, 27]]), 100)
+    e.run(w, (50, 50, 50))
+    p = grid.inner(e.pressure()).astype(np.float64)
+    assert abs(np.sqrt((p ** 2).sum()) / g["p_norm"] - 1) < 1e-6
+    assert abs(np.abs(p).max() / g["p_max"] - 1) < 1e-6
+
+
+def test_device_loop_equals_host_loop(mm):
+    """mm_cd_run (device wavelet/counter/recording) == step()+record() calls."""
+    g = load_golden("eng_cpml_aniso")
+    n = tuple(int(x) for x in g["n"])
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0))
+    opts = mm.EngineOptions(ndamping=tuple(int(x) for x in g["ndamping"]), taper=True)
+    rec = np.array([[i, j, 7] for i in range(n[0]) for j in range(0, n[1], 3)])
+    out = []
+    for use_loop in (False, True):
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, g["vp"], opts, float(g["dt"]),
+                                float(g["vmax"]), mode="strict")
+        e.set_receivers(rec, int(g["steps"]))
+        src = tuple(int(x) for x in g["src"])
+        if use_loop:
+            e.run(g["wavelet"], src)
+        else:
+            for s in range(int(g["steps"])):
+                e.step(float(g["wavelet"][s]), src)
+                e.record(s)
+        out.append((e.pressure(), e.traces()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[1][0], g["p_cur"])
