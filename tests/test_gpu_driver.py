@@ -40,7 +40,8 @@ def test_run_oracle_config_100(mm, mode):
     got = rec.traces[g["pick"]]
     if mode == "strict":
         assert np.array_equal(got, g["traces"])
-        assert abs(np.linalg.norm(rec.traces.astype(np.float64)) - g["trace_norm"]) == 0
+        # (float64 norm: summation order differs across hosts, hence 1e-12)
+        assert abs(np.linalg.norm(rec.traces.astype(np.float64)) / g["trace_norm"] - 1) < 1e-12
     else:
         assert rel_l2(got, g["traces"]) <= 1e-5
         assert abs(np.linalg.norm(rec.traces.astype(np.float64)) / g["trace_norm"] - 1) < 1e-5
