@@ -102,10 +102,8 @@ struct mm_cd_engine {
     DevBuf<float> cv, vp;
     // CPML
     DevBuf<float> ta[3], tb[3], tik[3];
-    DevBuf<int> map[3], list[3];
-    int cnt[3] = {0, 0, 0};
-    DevBuf<float> psi[3], zeta[3];
-    long long cs1[3] = {0, 0, 0}, cs2[3] = {0, 0, 0};
+    CpmlRun run[3][2] = {};
+    DevBuf<float> psi[3][2], zeta[3][2];
     // receivers / driver
     std::vector<int> rec_ijk;
     DevBuf<long long> rec_offs;
@@ -127,13 +125,8 @@ struct mm_cd_engine {
             s.ta[a] = ta[a].ptr;
             s.tb[a] = tb[a].ptr;
             s.tik[a] = tik[a].ptr;
-            s.map[a] = map[a].ptr;
-            s.list[a] = list[a].ptr;
-            s.cnt[a] = cnt[a];
-            s.psi[a] = psi[a].ptr;
-            s.zeta[a] = zeta[a].ptr;
-            s.cs1[a] = cs1[a];
-            s.cs2[a] = cs2[a];
+            s.run[a][0] = run[a][0];
+            s.run[a][1] = run[a][1];
             for (int m = 0; m < kMaxR; ++m) {
                 s.c2[a][m] = c2[a][m];
                 s.c1[a][m] = c1[a][m];
@@ -146,44 +139,60 @@ struct mm_cd_engine {
         return s;
     }
 
-    // Local tables + active-index maps + compact CPML storage from prof.
+    // Local tables + the CPML memory runs (one per damping layer and axis,
+    // allocated only where some a != 0) from prof.
     void setup_cpml() {
+        const long long nx4 = (lay.n[0] + 3) / 4 * 4;
         for (int ax = 0; ax < 3; ++ax) {
             const int n = lay.n[ax];
             std::vector<float> a(n), b(n), k(n);
-            std::vector<int> mp(n, -1), ls;
             for (int l = 0; l < n; ++l) {
                 const int g = l + goff[ax];
                 a[l] = prof.a[ax][g];
                 b[l] = prof.b[ax][g];
                 k[l] = prof.ik[ax][g];
-                if (a[l] != 0.0f) {
-                    mp[l] = (int)ls.size();
-                    ls.push_back(l);
-                }
             }
-            cnt[ax] = (int)ls.size();
             ta[ax].upload(a.data(), n, stream);
             tb[ax].upload(b.data(), n, stream);
             tik[ax].upload(k.data(), n, stream);
-            map[ax].upload(mp.data(), n, stream);
-            if (ls.empty()) ls.push_back(0);  // keep a valid pointer
-            list[ax].upload(ls.data(), ls.size(), stream);
-        }
-        const long long nx4 = (lay.n[0] + 3) / 4 * 4;
-        const long long w0 = (cnt[0] + 3) / 4 * 4;
-        cs1[0] = w0;
-        cs2[0] = w0 * lay.n[1];
-        cs1[1] = nx4;
-        cs2[1] = nx4 * cnt[1];
-        cs1[2] = nx4;
-        cs2[2] = nx4 * lay.n[1];
-        const size_t sz[3] = {(size_t)(cnt[0] ? cs2[0] * lay.n[2] : 0),
-                              (size_t)(cnt[1] ? cs2[1] * lay.n[2] : 0),
-                              (size_t)(cnt[2] ? cs2[2] * cnt[2] : 0)};
-        for (int ax = 0; ax < 3; ++ax) {
-            psi[ax].alloc_zero(sz[ax], stream);
-            zeta[ax].alloc_zero(sz[ax], stream);
+            // global layers [0, nd) and [gn - nd, gn), clipped to the local box
+            const int glo[2] = {0, gn[ax] - nd[ax]}, ghi[2] = {nd[ax], gn[ax]};
+            for (int side = 0; side < 2; ++side) {
+                CpmlRun& r = run[ax][side];
+                r = CpmlRun{0, 0, 0, nullptr, nullptr, 0, 0};
+                psi[ax][side].reset();
+                zeta[ax][side].reset();
+                const int lo = std::max(glo[side] - goff[ax], 0);
+                const int hi = std::min(ghi[side] - goff[ax], n);
+                bool active = false;
+                for (int l = lo; l < hi; ++l) active |= a[l] != 0.0f;
+                if (hi <= lo || !active) continue;
+                const long long w = hi - lo;
+                r.lo = lo;
+                r.hi = hi;
+                r.org = ax == 0 ? (lo & ~3) : lo;
+                size_t count;
+                if (ax == 0) {
+                    // rows start 16-byte aligned in x and are at least as wide as
+                    // the fast kernel's TMA boxes; padding columns stay zero (they
+                    // are part of the zero halo)
+                    r.s1 = std::max<long long>((hi - r.org + 3) / 4 * 4, 64);
+                    r.s2 = r.s1 * lay.n[1];
+                    count = (size_t)r.s2 * lay.n[2];
+                } else if (ax == 1) {
+                    r.s1 = nx4;
+                    r.s2 = nx4 * w;
+                    count = (size_t)r.s2 * lay.n[2];
+                } else {
+                    r.s1 = nx4;
+                    r.s2 = nx4 * lay.n[1];
+                    count = (size_t)r.s2 * w;
+                }
+                psi[ax][side].alloc_zero(count, stream);
+                zeta[ax][side].alloc_zero(count, stream);
+                r.psi = psi[ax][side].ptr;
+                r.zeta = zeta[ax][side].ptr;
+            }
         }
     }
 
@@ -478,7 +487,10 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     launch_velocity_coeff(e->vp.ptr, e->cv.ptr, e->dt2, L.total, e->stream);
     e->setup_cpml();
     e->counters.alloc_zero(2, e->stream);
-    if (mode == MM_MODE_FAST) e->fast = make_fast_plan(e->lay, device);
+    if (mode == MM_MODE_FAST) {
+        float* const bufs[3] = {e->p[0].ptr, e->p[1].ptr, e->p[2].ptr};
+        e->fast = make_fast_plan(e->lay, device, bufs, e->cv.ptr);
+    }
     MM_CUDA(cudaStreamSynchronize(e->stream));
     *out = e.release();
     MM_API_END

@@ -1,0 +1,92 @@
+// fast_common.cuh -- PTX helpers (mbarrier, TMA) shared by the fast kernels.
+#pragma once
+
+#include <cuda.h>
+
+#include "mm_internal.hpp"
+
+namespace mmb {
+namespace fast {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MM_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra MM_WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// 3D tiled TMA load global -> shared, completion counted on `bar` (bytes).
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            int z, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Dynamic work queue shared by the persistent kernels.  Items are ordered so
+// that the ~gridDim.x items in flight at any moment are spatial neighbours at
+// the same z (their halos meet in L2).  ctr[0] = next item, ctr[1] = CTAs
+// done; the last CTA resets both, so every launch / graph replay starts at 0.
+struct WorkQueue {
+    int* ctr;
+    int nitems;
+};
+__device__ __forceinline__ int wq_next(const WorkQueue& q, int* s_slot) {
+    if (threadIdx.x == 0) *s_slot = atomicAdd(q.ctr, 1);
+    __syncthreads();
+    const int v = *s_slot;
+    __syncthreads();
+    return v;
+}
+__device__ __forceinline__ void wq_done(const WorkQueue& q) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(q.ctr + 1, 1) == (int)gridDim.x - 1) {
+            atomicExch(q.ctr, 0);
+            atomicExch(q.ctr + 1, 0);
+        }
+    }
+}
+
+// Shared-memory region sizes rounded up to 128 bytes (32 floats): TMA
+// destinations must be 128-byte aligned.
+__host__ __device__ constexpr int pad32(int n) { return (n + 31) / 32 * 32; }
+
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float comp(const float4& v, int e) {
+    return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
+// Per-axis second-derivative term in the chosen association order.
+//  ORD 1: reference order with FMA: t = fma(c_m, (p+ + p-) - 2 p0, t)
+//  ORD 0: factored: t = fma(c_m, p+ + p-, t), centre added once by the caller
+template <int ORD>
+__device__ __forceinline__ float d2_term(float t, float c, float pp, float pm, float two_p0) {
+    if (ORD == 1) return fmaf(c, (pp + pm) - two_p0, t);
+    return fmaf(c, pp + pm, t);
+}
+
+}  // namespace fast
+}  // namespace mmb

@@ -1,8 +1,552 @@
-// kernels_fast.cu -- MM_MODE_FAST step kernels (placeholder until the TMA kernels land).
+// kernels_fast.cu -- MM_MODE_FAST step: plan (tensor maps, work lists) + launches.
+//
+// One step = pass 1 (psi) -> boundary (CPML pass 2) on the main stream, the
+// interior kernel concurrently on a side stream (it needs no CPML state),
+// then the source injection after the join.  The interior and boundary
+// kernels are persistent: their grids split the GPU's CTA slots in
+// proportion to their algorithmic bytes so both finish together.
+// Kernels: fast_inner.cuh (k_inner), fast_boundary.cuh (k_bnd, k_pass1).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "fast_boundary.cuh"
+#include "fast_inner.cuh"
 #include "mm_fast.hpp"
 
 namespace mmb {
 
-std::unique_ptr<FastPlan> make_fast_plan(const Layout&, int) { return nullptr; }
+namespace {
+
+using namespace fast;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    if (!fn) raise(ST_CUDA, "cuTensorMapEncodeTiled is unavailable");
+    return fn;
+}
+
+// 3D fp32 tensor map, x fastest; OOB elements read as zero.
+CUtensorMap make_map(const void* base, long long dx, long long dy, long long dz,
+                     long long row_floats, long long plane_floats, int bx, int by) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    if (!base) return m;  // absent run: never dereferenced
+    const cuuint64_t dims[3] = {(cuuint64_t)dx, (cuuint64_t)dy, (cuuint64_t)dz};
+    const cuuint64_t strides[2] = {(cuuint64_t)row_floats * 4, (cuuint64_t)plane_floats * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    // L2 promotion: 128B by default (boxes start 16B- but not always
+    // 256B-aligned; 256B promotion would fetch unused bytes).  MM_L2PROMO=0..3
+    // selects none/64B/128B/256B for experiments.
+    static const CUtensorMapL2promotion promo = [] {
+        const char* e = std::getenv("MM_L2PROMO");
+        const int v = e ? std::atoi(e) : 2;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+               : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                        : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    }();
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base),
+                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(ST_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+CUtensorMap field_map(const Layout& L, const float* base, int bx, int by) {
+    return make_map(base, L.P, L.ey, L.ez, L.P, L.plane, bx, by);
+}
+
+// Tensor map over one CPML run array (see CpmlRun in mm_internal.hpp).
+CUtensorMap run_map(const Layout& L, const CpmlRun& r, int ax, const float* base, int bx, int by) {
+    if (r.hi <= r.lo || !base) return make_map(nullptr, 0, 0, 0, 0, 0, 0, 0);
+    const long long w = r.hi - r.lo;
+    if (ax == 0) return make_map(base, r.s1, L.n[1], L.n[2], r.s1, r.s2, bx, by);
+    if (ax == 1) return make_map(base, r.s1, w, L.n[2], r.s1, r.s2, bx, by);
+    return make_map(base, r.s1, L.n[1], w, r.s1, r.s2, bx, by);
+}
+
+template <typename T>
+struct DArr {
+    T* ptr = nullptr;
+    size_t n = 0;
+    DArr() = default;
+    DArr(const DArr&) = delete;
+    DArr& operator=(const DArr&) = delete;
+    DArr(DArr&& o) noexcept : ptr(o.ptr), n(o.n) { o.ptr = nullptr; }
+    ~DArr() {
+        if (ptr) cudaFree(ptr);
+    }
+    void set(const std::vector<T>& v, cudaStream_t s) {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        n = v.size();
+        if (n == 0) return;
+        MM_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+        MM_CUDA(cudaMemcpyAsync(ptr, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+        MM_CUDA(cudaStreamSynchronize(s));
+    }
+};
+
+struct Box {
+    int lo[3], hi[3];
+};
+
+// Work items for the persistent kernels: each (tile, z-chunk) is one item.
+// Items are ordered chunk-major (all tiles of chunk 0, then chunk 1, ...) and
+// handed out dynamically (WorkQueue), so the items in flight at any moment are
+// neighbouring tiles at the same z and their halo planes meet in L2.  The
+// chunk length is chosen so that every CTA gets about one or more waves of
+// ~48-plane items.
+struct Item {
+    int tag, ty, zlo, zhi;
+};
+void wave_items(const std::vector<Item>& tiles, int ctas, std::vector<int4>& out) {
+    out.clear();
+    if (tiles.empty()) return;
+    long long tp = 0;
+    int zmax = 0;
+    for (const auto& t : tiles) {
+        tp += t.zhi - t.zlo;
+        zmax = std::max(zmax, t.zhi - t.zlo);
+    }
+    const double per_cta = (double)tp / std::max(1, ctas);
+    const int waves = std::max(1, (int)std::lround(per_cta / 48.0));
+    const int zc = std::max(4, (int)((tp + (long long)ctas * waves - 1) / ((long long)ctas * waves)));
+    for (int k = 0; (long long)k * zc < zmax; ++k)
+        for (const auto& t : tiles) {
+            const int zb = t.zlo + k * zc;
+            if (zb >= t.zhi) continue;
+            out.push_back(make_int4(t.tag, t.ty, zb, std::min(t.zhi, zb + zc)));
+        }
+}
+
+template <int R>
+class FastPlanR final : public FastPlan {
+    using IC = InnerCfg<R>;
+    using BC = BndCfg<R>;
+    static constexpr bool kBnd = BC::SMEM <= 200 * 1024;  // TMA boundary kernel fits
+
+public:
+    FastPlanR(const Layout& lay, int device, float* const bufs[3], const float* cv)
+        : lay_(lay), device_(device) {
+        for (int b = 0; b < 3; ++b) {
+            bufs_[b] = bufs[b];
+            in_halo_[b] = field_map(lay, bufs[b], IC::BX, IC::BY);
+            in_tile_[b] = field_map(lay, bufs[b], IC::TX, IC::TY);
+            bd_halo_[b] = field_map(lay, bufs[b], BC::BX, BC::BY);
+            bd_tile_[b] = field_map(lay, bufs[b], BC::TX, BC::TY);
+        }
+        cv_in_ = field_map(lay, cv, IC::TX, IC::TY);
+        cv_bd_ = field_map(lay, cv, BC::TX, BC::TY);
+        const char* ord = std::getenv("MM_FAST_ORDER");
+        order_ = ord && ord[0] == '0' ? 0 : 1;
+        const char* conc = std::getenv("MM_CONCURRENT");
+        concurrent_ = conc && conc[0] == '1';
+        cudaDeviceProp prop;
+        MM_CUDA(cudaGetDeviceProperties(&prop, device));
+        sms_ = prop.multiProcessorCount;
+        MM_CUDA(cudaFuncSetAttribute(k_inner<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)IC::SMEM));
+        MM_CUDA(cudaFuncSetAttribute(k_inner<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)IC::SMEM));
+        int per_sm = 0;
+        MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inner<R, 1>, IC::NT,
+                                                              IC::SMEM));
+        inner_per_sm_ = std::max(1, per_sm);
+        if constexpr (kBnd) {
+            MM_CUDA(cudaFuncSetAttribute(k_bnd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)BC::SMEM));
+            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bnd<R>, BC::NT,
+                                                                  BC::SMEM));
+            bnd_per_sm_ = std::max(1, per_sm);
+        }
+        MM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+        MM_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+        MM_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
+    }
+    ~FastPlanR() override {
+        cudaEventDestroy(fork_);
+        cudaEventDestroy(join_);
+        cudaStreamDestroy(side_);
+    }
+
+    void pass1(const StepParams& p, cudaStream_t s) override { launch_pass1(p, 0, lay_.n[2], s); }
+
+    void update(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t s) override {
+        if (region == 0) {
+            MM_CUDA(cudaEventRecord(fork_, s));
+            MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+            launch_inner(p, z_lo, z_hi, true, side_);
+            launch_boundary(p, z_lo, z_hi, true, s);
+            MM_CUDA(cudaEventRecord(join_, side_));
+            MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
+        } else if (region == 1) {
+            launch_inner(p, z_lo, z_hi, false, s);
+        } else {
+            launch_boundary(p, z_lo, z_hi, false, s);
+        }
+    }
+
+    void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
+              const int* step_dev, cudaStream_t s) override {
+        if (!concurrent_) {  // default: each kernel gets the whole GPU, in turn
+            launch_pass1(p, 0, lay_.n[2], s);
+            launch_boundary(p, 0, lay_.n[2], false, s);
+            launch_inner(p, 0, lay_.n[2], false, s);
+            if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
+            return;
+        }
+        MM_CUDA(cudaEventRecord(fork_, s));
+        MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+        launch_inner(p, 0, lay_.n[2], true, side_);
+        launch_pass1(p, 0, lay_.n[2], s);
+        launch_boundary(p, 0, lay_.n[2], true, s);
+        MM_CUDA(cudaEventRecord(join_, side_));
+        MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
+        if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
+    }
+
+private:
+    int buf_index(const float* ptr) const {
+        for (int b = 0; b < 3; ++b)
+            if (bufs_[b] == ptr) return b;
+        raise(ST_INVAL, "unknown pressure buffer");
+    }
+
+    // inner box + the six slab boxes of the local grid (grid.cpp:34-41)
+    void regions(const StepParams& p, Box& inner, std::vector<std::pair<int, Box>>& slabs) const {
+        int ilo[3], ihi[3];
+        for (int a = 0; a < 3; ++a) {
+            ilo[a] = std::max(p.nd[a] - p.goff[a], 0);
+            ihi[a] = std::min(p.gn[a] - p.nd[a] - p.goff[a], lay_.n[a]);
+            ihi[a] = std::max(ihi[a], ilo[a]);
+        }
+        const int n0 = lay_.n[0], n1 = lay_.n[1], n2 = lay_.n[2];
+        inner = Box{{ilo[0], ilo[1], ilo[2]}, {ihi[0], ihi[1], ihi[2]}};
+        // first = 2 * kind + side (kind 0/1/2 = X/Y/Z slab, side 0/1 = low/high)
+        const std::pair<int, Box> cand[6] = {
+            {0, Box{{0, 0, 0}, {ilo[0], n1, n2}}},
+            {1, Box{{ihi[0], 0, 0}, {n0, n1, n2}}},
+            {2, Box{{ilo[0], 0, 0}, {ihi[0], ilo[1], n2}}},
+            {3, Box{{ilo[0], ihi[1], 0}, {ihi[0], n1, n2}}},
+            {4, Box{{ilo[0], ilo[1], 0}, {ihi[0], ihi[1], ilo[2]}}},
+            {5, Box{{ilo[0], ilo[1], ihi[2]}, {ihi[0], ihi[1], n2}}},
+        };
+        slabs.clear();
+        for (const auto& b : cand)
+            if (b.second.hi[0] > b.second.lo[0] && b.second.hi[1] > b.second.lo[1] &&
+                b.second.hi[2] > b.second.lo[2])
+                slabs.push_back(b);
+    }
+
+    struct Work {
+        DArr<int4> segs;
+        DArr<int> ctr;  // WorkQueue counters
+        int nitems = 0;
+        int ctas = 0;
+        bool empty = true;
+        Box box{};
+        int x_base = 0;
+        BndBox bboxes[6];
+        int nbox = 0;
+    };
+
+    // CTA budgets.  Alone, a kernel gets every SM; when the interior and
+    // boundary kernels run concurrently the SMs are split in proportion to
+    // their algorithmic bytes so both finish together.
+    void budgets(const StepParams& p, int z_lo, int z_hi, bool conc, int& gi, int& gb) const {
+        if (!conc) {
+            gi = sms_ * inner_per_sm_;
+            gb = sms_ * bnd_per_sm_;
+            return;
+        }
+        Box inner;
+        std::vector<std::pair<int, Box>> slabs;
+        regions(p, inner, slabs);
+        auto vol = [&](const Box& b) {
+            const long long zl = std::max(b.lo[2], z_lo), zh = std::min(b.hi[2], z_hi);
+            if (zh <= zl) return 0.0;
+            return (double)(b.hi[0] - b.lo[0]) * (b.hi[1] - b.lo[1]) * (zh - zl);
+        };
+        const double wi = 16.0 * vol(inner);
+        double wb = 0;
+        for (const auto& s : slabs) wb += 34.0 * vol(s.second);
+        if (!kBnd) wb *= 4.0;  // strict boundary kernel is slower
+        if (wb <= 0) {
+            gi = sms_ * inner_per_sm_;
+            gb = 0;
+        } else if (wi <= 0) {
+            gi = 0;
+            gb = sms_ * bnd_per_sm_;
+        } else {
+            const int si = std::min(sms_ - 1,
+                                    std::max(1, (int)std::lround(sms_ * wi / (wi + wb))));
+            gi = si * inner_per_sm_;
+            gb = (sms_ - si) * bnd_per_sm_;
+        }
+    }
+
+    static long long wkey(int z_lo, int z_hi, bool conc) {
+        return ((long long)z_lo << 32) ^ ((long long)z_hi << 1) ^ (conc ? 1 : 0);
+    }
+
+    void finish_work(Work& w, const std::vector<Item>& tiles, int ctas) {
+        std::vector<int4> items;
+        wave_items(tiles, ctas, items);
+        w.nitems = (int)items.size();
+        w.ctas = std::max(1, std::min(ctas, w.nitems));
+        w.segs.set(items, stream_setup_);
+        w.ctr.set(std::vector<int>{0, 0}, stream_setup_);
+    }
+
+    Work& inner_work(const StepParams& p, int z_lo, int z_hi, bool conc) {
+        const auto key = wkey(z_lo, z_hi, conc);
+        auto it = inner_cache_.find(key);
+        if (it != inner_cache_.end()) return it->second;
+        Work& w = inner_cache_[key];
+        Box inner;
+        std::vector<std::pair<int, Box>> slabs;
+        regions(p, inner, slabs);
+        inner.lo[2] = std::max(inner.lo[2], z_lo);
+        inner.hi[2] = std::min(inner.hi[2], z_hi);
+        w.box = inner;
+        if (inner.hi[0] <= inner.lo[0] || inner.hi[1] <= inner.lo[1] || inner.hi[2] <= inner.lo[2])
+            return w;
+        w.empty = false;
+        w.x_base = inner.lo[0] & ~3;
+        const int tiles_x = (inner.hi[0] - w.x_base + IC::TX - 1) / IC::TX;
+        const int tiles_y = (inner.hi[1] - inner.lo[1] + IC::TY - 1) / IC::TY;
+        std::vector<Item> tiles;
+        for (int ty = 0; ty < tiles_y; ++ty)
+            for (int tx = 0; tx < tiles_x; ++tx)
+                tiles.push_back(Item{tx, ty, inner.lo[2], inner.hi[2]});
+        int gi, gb;
+        budgets(p, z_lo, z_hi, conc, gi, gb);
+        finish_work(w, tiles, std::max(1, gi));
+        return w;
+    }
+
+    Work& bnd_work(const StepParams& p, int z_lo, int z_hi, bool conc) {
+        const auto key = wkey(z_lo, z_hi, conc);
+        auto it = bnd_cache_.find(key);
+        if (it != bnd_cache_.end()) return it->second;
+        Work& w = bnd_cache_[key];
+        Box inner;
+        std::vector<std::pair<int, Box>> slabs;
+        regions(p, inner, slabs);
+        std::vector<Item> items;  // one per tile
+        w.nbox = 0;
+        for (const auto& s : slabs) {
+            const Box& b = s.second;
+            const int zl = std::max(b.lo[2], z_lo), zh = std::min(b.hi[2], z_hi);
+            if (zh <= zl) continue;
+            BndBox& bb = w.bboxes[w.nbox];
+            for (int a = 0; a < 3; ++a) {
+                bb.lo[a] = b.lo[a];
+                bb.hi[a] = b.hi[a];
+            }
+            bb.kind = s.first / 2;
+            bb.side = s.first % 2;
+            bb.x_base = b.lo[0] & ~3;
+            const int tiles_x = (b.hi[0] - bb.x_base + BC::TX - 1) / BC::TX;
+            const int tiles_y = (b.hi[1] - b.lo[1] + BC::TY - 1) / BC::TY;
+            for (int ty = 0; ty < tiles_y; ++ty)
+                for (int tx = 0; tx < tiles_x; ++tx)
+                    items.push_back(Item{w.nbox | (tx << 3), ty, zl, zh});
+            ++w.nbox;
+        }
+        if (items.empty()) return w;
+        w.empty = false;
+        int gi, gb;
+        budgets(p, z_lo, z_hi, conc, gi, gb);
+        finish_work(w, items, std::max(1, gb));
+        return w;
+    }
+
+    void launch_inner(const StepParams& p, int z_lo, int z_hi, bool conc, cudaStream_t s) {
+        Work& w = inner_work(p, z_lo, z_hi, conc);
+        if (w.empty) return;
+        InnerParams ip;
+        std::memset(&ip, 0, sizeof ip);
+        ip.lay = lay_;
+        for (int a = 0; a < 3; ++a) {
+            ip.lo[a] = w.box.lo[a];
+            ip.hi[a] = w.box.hi[a];
+        }
+        ip.x_base = w.x_base;
+        ip.segs = w.segs.ptr;
+        ip.wq = WorkQueue{w.ctr.ptr, w.nitems};
+        ip.pn = p.pn;
+        float sum = 0.0f;
+        for (int m = 0; m < R; ++m) {
+            ip.cx[m] = p.c2[0][m];
+            ip.cy[m] = p.c2[1][m];
+            ip.cz[m] = p.c2[2][m];
+            sum += p.c2[0][m] + p.c2[1][m] + p.c2[2][m];
+        }
+        ip.center = -2.0f * sum;
+        const int bc = buf_index(p.pc), bp = buf_index(p.pp);
+        if (order_ == 1)
+            k_inner<R, 1><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
+        else
+            k_inner<R, 0><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
+        note_launches(1);
+        MM_CUDA(cudaGetLastError());
+    }
+
+    void refresh_run_maps(const StepParams& p) {
+        bool same = true;
+        for (int a = 0; a < 3; ++a)
+            for (int sd = 0; sd < 2; ++sd)
+                same = same && p.run[a][sd].psi == runs_[a][sd].psi &&
+                       p.run[a][sd].zeta == runs_[a][sd].zeta;
+        if (same && runs_valid_) return;
+        for (int a = 0; a < 3; ++a)
+            for (int sd = 0; sd < 2; ++sd) {
+                const CpmlRun& r = p.run[a][sd];
+                runs_[a][sd] = r;
+                int bx = BC::TX, by = BC::TY;
+                if (a == 0) bx = BC::BX;  // x halo
+                if (a == 1) by = BC::BY;  // y halo
+                maps_.psi[a][sd] = run_map(lay_, r, a, r.psi, bx, by);
+                maps_.zeta[a][sd] = run_map(lay_, r, a, r.zeta, BC::TX, BC::TY);
+            }
+        runs_valid_ = true;
+    }
+
+    void launch_boundary(const StepParams& p, int z_lo, int z_hi, bool conc, cudaStream_t s) {
+        if constexpr (!kBnd) {
+            strict_update(p, 2, z_lo, z_hi, s);
+            return;
+        } else {
+            Work& w = bnd_work(p, z_lo, z_hi, conc);
+            if (w.empty) return;
+            refresh_run_maps(p);
+            const int bc = buf_index(p.pc), bp = buf_index(p.pp);
+            maps_.pc = bd_halo_[bc];
+            maps_.pp = bd_tile_[bp];
+            maps_.cv = cv_bd_;
+            BndParams bp_;
+            std::memset(&bp_, 0, sizeof bp_);
+            bp_.lay = lay_;
+            for (int i = 0; i < w.nbox; ++i) bp_.box[i] = w.bboxes[i];
+            bp_.nbox = w.nbox;
+            for (int a = 0; a < 3; ++a) {
+                bp_.run[a][0] = p.run[a][0];
+                bp_.run[a][1] = p.run[a][1];
+                bp_.ta[a] = p.ta[a];
+                bp_.tb[a] = p.tb[a];
+                bp_.tik[a] = p.tik[a];
+                for (int m = 0; m < kMaxR; ++m) {
+                    bp_.c2[a][m] = p.c2[a][m];
+                    bp_.c1[a][m] = p.c1[a][m];
+                }
+            }
+            bp_.pn = p.pn;
+            bp_.segs = w.segs.ptr;
+            bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
+            k_bnd<R><<<w.ctas, BC::NT, BC::SMEM, s>>>(maps_, bp_);
+            note_launches(1);
+            MM_CUDA(cudaGetLastError());
+        }
+    }
+
+    void launch_pass1(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) {
+        if constexpr (!kBnd) {
+            strict_pass1(p, z_lo, z_hi, s);
+            return;
+        } else {
+            const auto key = std::make_pair(z_lo, z_hi);
+            auto it = pass1_cache_.find(key);
+            if (it == pass1_cache_.end()) {
+                std::vector<RunDesc> runs;
+                std::vector<int4> items;
+                for (int ax = 0; ax < 3; ++ax)
+                    for (int side = 0; side < 2; ++side) {
+                        const CpmlRun& r = p.run[ax][side];
+                        if (r.hi <= r.lo) continue;
+                        RunDesc d{ax, side, {0, 0, 0}, {lay_.n[0], lay_.n[1], lay_.n[2]}, 0};
+                        d.lo[ax] = r.lo;
+                        d.hi[ax] = r.hi;
+                        d.lo[2] = std::max(d.lo[2], z_lo);
+                        d.hi[2] = std::min(d.hi[2], z_hi);
+                        if (d.hi[2] <= d.lo[2]) continue;
+                        d.x_base = d.lo[0] & ~3;
+                        const int ri = (int)runs.size();
+                        runs.push_back(d);
+                        const int tx = (d.hi[0] - d.x_base + 31) / 32;
+                        const int ty = (d.hi[1] - d.lo[1] + 31) / 32;
+                        const int zc = ax == 2 ? d.hi[2] - d.lo[2] : 16;
+                        for (int zb = d.lo[2]; zb < d.hi[2]; zb += zc)
+                            for (int b = 0; b < ty; ++b)
+                                for (int a = 0; a < tx; ++a)
+                                    items.push_back(make_int4(ri | (a << 4), b, zb,
+                                                              std::min(d.hi[2], zb + zc)));
+                    }
+                auto& e = pass1_cache_[key];
+                e.runs.set(runs, stream_setup_);
+                e.items.set(items, stream_setup_);
+                e.count = (int)items.size();
+                it = pass1_cache_.find(key);
+            }
+            auto& e = it->second;
+            if (e.count == 0) return;
+            k_pass1<R><<<e.count, 256, 0, s>>>(p, e.runs.ptr, e.items.ptr, e.count);
+            note_launches(1);
+            MM_CUDA(cudaGetLastError());
+        }
+    }
+
+    struct Pass1Work {
+        DArr<RunDesc> runs;
+        DArr<int4> items;
+        int count = 0;
+    };
+
+    Layout lay_;
+    int device_;
+    int sms_ = 148, inner_per_sm_ = 1, bnd_per_sm_ = 1;
+    int order_ = 1;
+    bool concurrent_ = false;  // MM_CONCURRENT=1: interior on a side stream, SMs split
+    const float* bufs_[3];
+    CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;
+    BndMaps maps_;
+    CpmlRun runs_[3][2] = {};
+    bool runs_valid_ = false;
+    cudaStream_t side_ = nullptr, stream_setup_ = nullptr;
+    cudaEvent_t fork_ = nullptr, join_ = nullptr;
+    std::map<long long, Work> inner_cache_, bnd_cache_;
+    std::map<std::pair<int, int>, Pass1Work> pass1_cache_;
+};
+
+}  // namespace
+
+std::unique_ptr<FastPlan> make_fast_plan(const Layout& lay, int device, float* const bufs[3],
+                                         const float* cv) {
+    switch (lay.r) {
+        case 2: return std::make_unique<FastPlanR<2>>(lay, device, bufs, cv);
+        case 4: return std::make_unique<FastPlanR<4>>(lay, device, bufs, cv);
+        case 8: return std::make_unique<FastPlanR<8>>(lay, device, bufs, cv);
+        default: return nullptr;  // other radii run the strict kernels
+    }
+}
 
 }  // namespace mmb

@@ -10,6 +10,7 @@
 // layer indices; the per-slab zero-halo semantics of the reference's
 // BoxArray (cpml.hpp:77-99) are reproduced by the slab mask below (see
 // DESIGN.md "CPML masking rule").
+#include <algorithm>
 #include <climits>
 
 #include "mm_internal.hpp"
@@ -33,23 +34,21 @@ __device__ __forceinline__ float d2_strict(const float* q, long long s, const fl
     return t;
 }
 
-__device__ __forceinline__ long long compact_off(const StepParams& p, int ax, int i, int j, int k,
-                                                 int ci) {
-    if (ax == 0) return ci + j * p.cs1[0] + k * p.cs2[0];
-    if (ax == 1) return i + ci * p.cs1[1] + k * p.cs2[1];
-    return i + j * p.cs1[2] + ci * p.cs2[2];
+// The CPML run of axis `ax` containing local coordinate l, or nullptr.
+__device__ __forceinline__ const CpmlRun* run_at(const StepParams& p, int ax, int l) {
+    if (l >= p.run[ax][0].lo && l < p.run[ax][0].hi) return &p.run[ax][0];
+    if (l >= p.run[ax][1].lo && l < p.run[ax][1].hi) return &p.run[ax][1];
+    return nullptr;
 }
 
-// psi_ax at local (i,j,k) shifted by `sh` along ax; zero outside the local
-// box or outside the active layer (the reference's zero halo).
+// psi_ax at local (i,j,k) shifted by `sh` along ax; zero outside the damping
+// runs and outside the local box (the reference's zero halo).
 __device__ __forceinline__ float psi_at(const StepParams& p, int ax, int i, int j, int k, int sh) {
     int loc[3] = {i, j, k};
     loc[ax] += sh;
-    const int l = loc[ax];
-    if (l < 0 || l >= p.lay.n[ax]) return 0.0f;
-    const int ci = __ldg(p.map[ax] + l);
-    if (ci < 0) return 0.0f;
-    return __ldg(p.psi[ax] + compact_off(p, ax, loc[0], loc[1], loc[2], ci));
+    const CpmlRun* r = run_at(p, ax, loc[ax]);
+    if (!r) return 0.0f;
+    return __ldg(r->psi + run_off(*r, ax, loc[0], loc[1], loc[2]));
 }
 
 template <int R>
@@ -96,10 +95,10 @@ __global__ void k_strict_update(StepParams p, int region, int z_lo) {
                                                                  psi_at(p, ax, i, j, k, -m))));
             }
             const float drive = fadd(fmul(d2p, ik), dpsi);
-            const int ci = __ldg(p.map[ax] + l);
+            const CpmlRun* run = run_at(p, ax, l);
             float z;
-            if (ci >= 0) {
-                float* zp = p.zeta[ax] + compact_off(p, ax, i, j, k, ci);
+            if (run) {
+                float* zp = run->zeta + run_off(*run, ax, i, j, k);
                 z = fadd(fmul(b, *zp), fmul(a, drive));
                 *zp = z;
             } else {
@@ -114,15 +113,14 @@ __global__ void k_strict_update(StepParams p, int region, int z_lo) {
 
 // Pass 1 over the compact storage of one axis: psi = b psi + a D1(p_cur).
 template <int R>
-__global__ void k_strict_pass1(StepParams p, int ax, int ext0, int ext1, int ext2, int z_lo,
-                               int z_hi) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    const int z = blockIdx.z;
-    if (x >= ext0 || y >= ext1 || z >= ext2) return;
-    int loc[3] = {x, y, z};
-    loc[ax] = __ldg(p.list[ax] + loc[ax]);
-    if (loc[2] < z_lo || loc[2] >= z_hi) return;
+__global__ void k_strict_pass1(StepParams p, int ax, int side, int z_lo) {
+    const CpmlRun& run = p.run[ax][side];
+    int loc[3] = {(int)(blockIdx.x * blockDim.x + threadIdx.x),
+                  (int)(blockIdx.y * blockDim.y + threadIdx.y), z_lo + (int)blockIdx.z};
+    loc[ax] += run.lo;
+    const int hi[3] = {ax == 0 ? run.hi : p.lay.n[0], ax == 1 ? run.hi : p.lay.n[1],
+                       ax == 2 ? run.hi : p.lay.n[2]};
+    if (loc[0] >= hi[0] || loc[1] >= hi[1] || loc[2] >= hi[2]) return;
     const long long s[3] = {1, p.lay.P, p.lay.plane};
     const float* q = p.pc + p.lay.off(loc[0], loc[1], loc[2]);
     float dp = 0.0f;
@@ -131,22 +129,26 @@ __global__ void k_strict_pass1(StepParams p, int ax, int ext0, int ext1, int ext
         dp = fadd(dp, fmul(p.c1[ax][m - 1], fsub(__ldg(q + m * s[ax]), __ldg(q - m * s[ax]))));
     const int l = loc[ax];
     const float a = __ldg(p.ta[ax] + l), b = __ldg(p.tb[ax] + l);
-    const int ci = ax == 0 ? x : ax == 1 ? y : z;
-    float* ps = p.psi[ax] + compact_off(p, ax, loc[0], loc[1], loc[2], ci);
+    float* ps = run.psi + run_off(run, ax, loc[0], loc[1], loc[2]);
     *ps = fadd(fmul(b, *ps), fmul(a, dp));
 }
 
 template <int R>
 void strict_pass1_r(const StepParams& p, int z_lo, int z_hi, cudaStream_t st) {
-    for (int ax = 0; ax < 3; ++ax) {
-        if (p.cnt[ax] == 0) continue;
-        int ext[3] = {p.lay.n[0], p.lay.n[1], p.lay.n[2]};
-        ext[ax] = p.cnt[ax];
-        dim3 blk(32, 8, 1);
-        dim3 grd((ext[0] + 31) / 32, (ext[1] + 7) / 8, ext[2]);
-        k_strict_pass1<R><<<grd, blk, 0, st>>>(p, ax, ext[0], ext[1], ext[2], z_lo, z_hi);
-        note_launches(1);
-    }
+    for (int ax = 0; ax < 3; ++ax)
+        for (int side = 0; side < 2; ++side) {
+            const CpmlRun& run = p.run[ax][side];
+            if (run.hi <= run.lo) continue;
+            int lo[3] = {0, 0, z_lo}, hi[3] = {p.lay.n[0], p.lay.n[1], z_hi};
+            lo[ax] = ax == 2 ? std::max(run.lo, z_lo) : run.lo;
+            hi[ax] = ax == 2 ? std::min(run.hi, z_hi) : run.hi;
+            if (hi[0] <= lo[0] || hi[1] <= lo[1] || hi[2] <= lo[2]) continue;
+            dim3 blk(32, 8, 1);
+            dim3 grd((hi[0] - lo[0] + 31) / 32, (hi[1] - lo[1] + 7) / 8, hi[2] - lo[2]);
+            // kernel coordinates: offset along ax is relative to run.lo
+            k_strict_pass1<R><<<grd, blk, 0, st>>>(p, ax, side, ax == 2 ? lo[2] - run.lo + 0 : lo[2]);
+            note_launches(1);
+        }
 }
 
 template <int R>

@@ -21,6 +21,7 @@ public:
 
 // nullptr when the fast kernels cannot serve this layout (the engine then
 // runs the strict kernels, which are exact for every radius).
-std::unique_ptr<FastPlan> make_fast_plan(const Layout& lay, int device);
+std::unique_ptr<FastPlan> make_fast_plan(const Layout& lay, int device, float* const bufs[3],
+                                         const float* cv);
 
 }  // namespace mmb

@@ -85,6 +85,29 @@ struct Layout {
 
 constexpr int kMaxR = 8;
 
+// CPML memory of one damping layer ("run") of one axis: the local index range
+// [lo, hi) along that axis, full extent along the other two.  Reads outside
+// the run return 0 -- the zero halo of the reference's per-slab BoxArray
+// (cpml.hpp:77-99).  Element (i,j,k), c = (axis coordinate) - lo:
+//   axis 0: c + j*s1 + k*s2      (s1 = W = round_up(hi-lo, 4), s2 = W*ny)
+//   axis 1: i + c*s1 + k*s2      (s1 = nx4, s2 = nx4*(hi-lo))
+//   axis 2: i + j*s1 + c*s2      (s1 = nx4, s2 = nx4*ny)
+// nx4 = round_up(nx, 4).  A run is allocated only if some a != 0 in it.
+struct CpmlRun {
+    int lo, hi;  // hi <= lo: absent
+    int org;     // array origin along the axis: lo, rounded down to 4 for axis 0
+                 // (TMA box starts must be 16-byte aligned in the fastest dim)
+    float* psi;
+    float* zeta;
+    long long s1, s2;
+};
+
+__host__ __device__ inline long long run_off(const CpmlRun& r, int ax, int i, int j, int k) {
+    if (ax == 0) return (i - r.org) + j * r.s1 + k * r.s2;
+    if (ax == 1) return i + (j - r.org) * r.s1 + k * r.s2;
+    return i + j * r.s1 + (k - r.org) * r.s2;
+}
+
 // Everything a step kernel needs, passed by value.
 struct StepParams {
     Layout lay;
@@ -97,16 +120,11 @@ struct StepParams {
     const float* cv;  // (dt2 * vp) * vp, device layout
     float c2[3][kMaxR];  // second-derivative taps per axis (float, 1/h^2 folded)
     float c1[3][kMaxR];  // central first-derivative taps per axis
-    // CPML: local tables (length n[ax]), active-index maps and compact storage
+    // CPML: local tables (length n[ax]) and the per-layer memory runs
     const float* ta[3];
     const float* tb[3];
     const float* tik[3];
-    const int* map[3];   // local index -> compact index, -1 if inactive (a == 0)
-    const int* list[3];  // compact index -> local index
-    int cnt[3];          // number of active indices per axis
-    float* psi[3];
-    float* zeta[3];
-    long long cs1[3], cs2[3];  // compact strides of y and z per axis (x stride 1)
+    CpmlRun run[3][2];  // [axis][0 = low layer, 1 = high layer]
 };
 
 // Receiver sampling, device trace layout [step][receiver].
