@@ -132,7 +132,7 @@ __device__ __forceinline__ int zrun_of(const BndParams& P, int z) {
     return in_run(P.run[2][0], z) ? 0 : in_run(P.run[2][1], z) ? 1 : -1;
 }
 
-template <int R>
+template <int R, int ORD>
 // Register cap for two CTAs of 8 warps per SM (see k_inner).
 __global__ void __maxnreg__(128)
     k_bnd(const __grid_constant__ BndMaps M, const BndParams P) {
@@ -360,8 +360,8 @@ __global__ void __maxnreg__(128)
                     for (int e = 0; e < PX; ++e)
 #pragma unroll
                         for (int m = 1; m <= R; ++m)
-                            dpx[e] = fmaf(P.c1[0][m - 1], ps[C::HX + e + m] - ps[C::HX + e - m],
-                                          dpx[e]);
+                            dpx[e] = acc<ORD>(dpx[e], P.c1[0][m - 1],
+                                              fs<ORD>(ps[C::HX + e + m], ps[C::HX + e - m]));
                 }
                 if (fy0 || fy1) {
                     const float* p0y = Q + C::O_PSY0 + (R + ty) * C::TX + PX * tx;
@@ -383,8 +383,8 @@ __global__ void __maxnreg__(128)
                             dn.x += b.x;
                             dn.y += b.y;
                         }
-                        dpy[0] = fmaf(P.c1[1][m - 1], up.x - dn.x, dpy[0]);
-                        dpy[1] = fmaf(P.c1[1][m - 1], up.y - dn.y, dpy[1]);
+                        dpy[0] = acc<ORD>(dpy[0], P.c1[1][m - 1], fs<ORD>(up.x, dn.x));
+                        dpy[1] = acc<ORD>(dpy[1], P.c1[1][m - 1], fs<ORD>(up.y, dn.y));
                     }
                 }
                 float2 zx = make_float2(0.f, 0.f), zy = zx, zz = zx;
@@ -396,8 +396,8 @@ __global__ void __maxnreg__(128)
                 ++nq;
 #pragma unroll
                 for (int m = 1; m <= R; ++m) {
-                    dpz[0] = fmaf(P.c1[2][m - 1], qz[R + m].x - qz[R - m].x, dpz[0]);
-                    dpz[1] = fmaf(P.c1[2][m - 1], qz[R + m].y - qz[R - m].y, dpz[1]);
+                    dpz[0] = acc<ORD>(dpz[0], P.c1[2][m - 1], fs<ORD>(qz[R + m].x, qz[R - m].x));
+                    dpz[1] = acc<ORD>(dpz[1], P.c1[2][m - 1], fs<ORD>(qz[R + m].y, qz[R - m].y));
                 }
                 float out[PX], nzx[PX], nzy[PX], nzz[PX];
 #pragma unroll
@@ -407,21 +407,24 @@ __global__ void __maxnreg__(128)
                     float d2x = 0.f, d2y = 0.f, d2z = 0.f;
 #pragma unroll
                     for (int m = 1; m <= R; ++m) {
-                        d2x = d2_term<1>(d2x, P.c2[0][m - 1], xs[C::HX + e + m], xs[C::HX + e - m],
-                                         two_p0);
-                        d2y = d2_term<1>(d2y, P.c2[1][m - 1], c2of(yu[m - 1], e),
-                                         c2of(yd[m - 1], e), two_p0);
-                        d2z = d2_term<1>(d2z, P.c2[2][m - 1], c2of(q[R + m], e),
-                                         c2of(q[R - m], e), two_p0);
+                        d2x = d2_term<ORD>(d2x, P.c2[0][m - 1], xs[C::HX + e + m],
+                                           xs[C::HX + e - m], two_p0);
+                        d2y = d2_term<ORD>(d2y, P.c2[1][m - 1], c2of(yu[m - 1], e),
+                                           c2of(yd[m - 1], e), two_p0);
+                        d2z = d2_term<ORD>(d2z, P.c2[2][m - 1], c2of(q[R + m], e),
+                                           c2of(q[R - m], e), two_p0);
                     }
-                    const float drx = fmaf(d2x, axk[e], dpx[e]);
-                    const float dry = fmaf(d2y, ayk, dpy[e]);
-                    const float drz = fmaf(d2z, azk, dpz[e]);
-                    nzx[e] = fx ? fmaf(axb[e], c2of(zx, e), axa[e] * drx) : 0.f;
-                    nzy[e] = y_in_zy ? fmaf(ayb, c2of(zy, e), aya * dry) : 0.f;
-                    nzz[e] = zr >= 0 ? fmaf(azb, c2of(zz, e), aza * drz) : 0.f;
-                    const float lap = ((drx + nzx[e]) + (dry + nzy[e])) + (drz + nzz[e]);
-                    out[e] = fmaf(c2of(cv, e), lap, two_p0 - c2of(pp, e));
+                    // reference: drive = d2p*ik + dpsi; zeta = b*zeta + a*drive;
+                    // term = drive + zeta; lap = (term_x + term_y) + term_z
+                    const float drx = acc<ORD>(dpx[e], d2x, axk[e]);
+                    const float dry = acc<ORD>(dpy[e], d2y, ayk);
+                    const float drz = acc<ORD>(dpz[e], d2z, azk);
+                    nzx[e] = fx ? acc<ORD>(fm<ORD>(axa[e], drx), axb[e], c2of(zx, e)) : 0.f;
+                    nzy[e] = y_in_zy ? acc<ORD>(fm<ORD>(aya, dry), ayb, c2of(zy, e)) : 0.f;
+                    nzz[e] = zr >= 0 ? acc<ORD>(fm<ORD>(aza, drz), azb, c2of(zz, e)) : 0.f;
+                    const float lap = fa<ORD>(fa<ORD>(fa<ORD>(drx, nzx[e]), fa<ORD>(dry, nzy[e])),
+                                              fa<ORD>(drz, nzz[e]));
+                    out[e] = acc<ORD>(fs<ORD>(two_p0, c2of(pp, e)), c2of(cv, e), lap);
                 }
                 // stores: p_next for points inside the box, zeta where a run holds them
                 float* dst = dst_base + (long long)o * L.plane;
@@ -460,7 +463,7 @@ struct RunDesc {
     int x_base;        // multiple of 4 (absolute x; run org is a multiple of 4)
 };
 
-template <int R>
+template <int R, int ORD>
 __global__ void __launch_bounds__(256)
     k_pass1(const StepParams p, const RunDesc* runs, const int4* items, int nitems) {
     const int it = blockIdx.x;
@@ -501,15 +504,16 @@ __global__ void __launch_bounds__(256)
     auto update = [&](float* ps, const float (&dp)[4], const float (&a)[4], const float (&b)[4]) {
         if (all) {
             float4 v = *reinterpret_cast<float4*>(ps);
-            v.x = fmaf(b[0], v.x, a[0] * dp[0]);
-            v.y = fmaf(b[1], v.y, a[1] * dp[1]);
-            v.z = fmaf(b[2], v.z, a[2] * dp[2]);
-            v.w = fmaf(b[3], v.w, a[3] * dp[3]);
+            // reference: psi = b * psi + a * dp
+            v.x = acc<ORD>(fm<ORD>(a[0], dp[0]), b[0], v.x);
+            v.y = acc<ORD>(fm<ORD>(a[1], dp[1]), b[1], v.y);
+            v.z = acc<ORD>(fm<ORD>(a[2], dp[2]), b[2], v.z);
+            v.w = acc<ORD>(fm<ORD>(a[3], dp[3]), b[3], v.w);
             *reinterpret_cast<float4*>(ps) = v;
         } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-                if (ok[e]) ps[e] = fmaf(b[e], ps[e], a[e] * dp[e]);
+                if (ok[e]) ps[e] = acc<ORD>(fm<ORD>(a[e], dp[e]), b[e], ps[e]);
         }
     };
     if (ax == 2) {
@@ -527,10 +531,10 @@ __global__ void __launch_bounds__(256)
             float dp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int m = 1; m <= R; ++m) {
-                dp[0] = fmaf(c1[m - 1], qq[R + m].x - qq[R - m].x, dp[0]);
-                dp[1] = fmaf(c1[m - 1], qq[R + m].y - qq[R - m].y, dp[1]);
-                dp[2] = fmaf(c1[m - 1], qq[R + m].z - qq[R - m].z, dp[2]);
-                dp[3] = fmaf(c1[m - 1], qq[R + m].w - qq[R - m].w, dp[3]);
+                dp[0] = acc<ORD>(dp[0], c1[m - 1], fs<ORD>(qq[R + m].x, qq[R - m].x));
+                dp[1] = acc<ORD>(dp[1], c1[m - 1], fs<ORD>(qq[R + m].y, qq[R - m].y));
+                dp[2] = acc<ORD>(dp[2], c1[m - 1], fs<ORD>(qq[R + m].z, qq[R - m].z));
+                dp[3] = acc<ORD>(dp[3], c1[m - 1], fs<ORD>(qq[R + m].w, qq[R - m].w));
             }
             const float az = __ldg(p.ta[2] + z), bz = __ldg(p.tb[2] + z);
             const float a4[4] = {az, az, az, az}, b4[4] = {bz, bz, bz, bz};
@@ -557,17 +561,17 @@ __global__ void __launch_bounds__(256)
             for (int e = 0; e < 4; ++e)
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
-                    dp[e] = fmaf(c1[m - 1], v[H + e + m] - v[H + e - m], dp[e]);
+                    dp[e] = acc<ORD>(dp[e], c1[m - 1], fs<ORD>(v[H + e + m], v[H + e - m]));
             update(run.psi + run_off(run, 0, x, y, z), dp, av, bv);
         } else {
 #pragma unroll
             for (int m = 1; m <= R; ++m) {
                 const float4 u = __ldg(reinterpret_cast<const float4*>(c + m * L.P));
                 const float4 d = __ldg(reinterpret_cast<const float4*>(c - m * L.P));
-                dp[0] = fmaf(c1[m - 1], u.x - d.x, dp[0]);
-                dp[1] = fmaf(c1[m - 1], u.y - d.y, dp[1]);
-                dp[2] = fmaf(c1[m - 1], u.z - d.z, dp[2]);
-                dp[3] = fmaf(c1[m - 1], u.w - d.w, dp[3]);
+                dp[0] = acc<ORD>(dp[0], c1[m - 1], fs<ORD>(u.x, d.x));
+                dp[1] = acc<ORD>(dp[1], c1[m - 1], fs<ORD>(u.y, d.y));
+                dp[2] = acc<ORD>(dp[2], c1[m - 1], fs<ORD>(u.z, d.z));
+                dp[3] = acc<ORD>(dp[3], c1[m - 1], fs<ORD>(u.w, d.w));
             }
             update(run.psi + run_off(run, 1, x, y, z), dp, av, bv);
         }

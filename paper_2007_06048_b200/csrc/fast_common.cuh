@@ -79,13 +79,35 @@ __device__ __forceinline__ float comp(const float4& v, int e) {
     return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
 }
 
-// Per-axis second-derivative term in the chosen association order.
-//  ORD 1: reference order with FMA: t = fma(c_m, (p+ + p-) - 2 p0, t)
-//  ORD 0: factored: t = fma(c_m, p+ + p-, t), centre added once by the caller
+// Arithmetic of the fast kernels, by association order ORD:
+//  ORD 2 (default): the reference's order with every operation separately
+//         rounded (no FMA contraction) -- bit-identical to the CPU reference
+//  ORD 1: reference order with FMA contraction
+//  ORD 0: factored stencil, t = fma(c_m, p+ + p-, t), centre added once
+template <int ORD>
+__device__ __forceinline__ float fa(float a, float b) {
+    return ORD == 2 ? __fadd_rn(a, b) : a + b;
+}
+template <int ORD>
+__device__ __forceinline__ float fs(float a, float b) {
+    return ORD == 2 ? __fsub_rn(a, b) : a - b;
+}
+template <int ORD>
+__device__ __forceinline__ float fm(float a, float b) {
+    return ORD == 2 ? __fmul_rn(a, b) : a * b;
+}
+// t + c * x  (reference: `t += c * x`)
+template <int ORD>
+__device__ __forceinline__ float acc(float t, float c, float x) {
+    return ORD == 2 ? __fadd_rn(t, __fmul_rn(c, x)) : fmaf(c, x, t);
+}
+
+// Per-axis second-derivative term (second_derivative_at, stencil.hpp:86-91):
+//   t += c_m * ((p[+m] + p[-m]) - 2 p0)
 template <int ORD>
 __device__ __forceinline__ float d2_term(float t, float c, float pp, float pm, float two_p0) {
-    if (ORD == 1) return fmaf(c, (pp + pm) - two_p0, t);
-    return fmaf(c, pp + pm, t);
+    if (ORD == 0) return fmaf(c, pp + pm, t);
+    return acc<ORD>(t, c, fs<ORD>(fa<ORD>(pp, pm), two_p0));
 }
 
 }  // namespace fast

@@ -170,19 +170,19 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, 1)
                         const float p0 = xs[C::HX + e];
                         const float two_p0 = 2.0f * p0;
                         float lap;
-                        if (ORD == 1) {
+                        if (ORD >= 1) {
                             float tx_ = 0.0f, ty_ = 0.0f, tz_ = 0.0f;
 #pragma unroll
                             for (int m = 1; m <= R; ++m) {
-                                tx_ = d2_term<1>(tx_, P.cx[m - 1], xs[C::HX + e + m],
+                                tx_ = d2_term<ORD>(tx_, P.cx[m - 1], xs[C::HX + e + m],
                                                  xs[C::HX + e - m], two_p0);
-                                ty_ = d2_term<1>(ty_, P.cy[m - 1], comp(yu[m - 1], e),
+                                ty_ = d2_term<ORD>(ty_, P.cy[m - 1], comp(yu[m - 1], e),
                                                  comp(yd[m - 1], e), two_p0);
-                                tz_ = d2_term<1>(tz_, P.cz[m - 1],
+                                tz_ = d2_term<ORD>(tz_, P.cz[m - 1],
                                                  comp(q[(CU + m) % C::QW], e),
                                                  comp(q[(CU + C::QW - m) % C::QW], e), two_p0);
                             }
-                            lap = (tx_ + ty_) + tz_;
+                            lap = fa<ORD>(fa<ORD>(tx_, ty_), tz_);
                         } else {
                             float t = P.center * p0;
 #pragma unroll
@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, 1)
                             }
                             lap = t;
                         }
-                        out[e] = fmaf(comp(cv, e), lap, two_p0 - comp(pp, e));
+                        out[e] = ORD == 2 ? __fadd_rn(__fsub_rn(two_p0, comp(pp, e)), __fmul_rn(comp(cv, e), lap))
+                                        : fmaf(comp(cv, e), lap, two_p0 - comp(pp, e));
                     }
                     if (yok) {
                         float* dst = dst_base + (long long)o * L.plane;

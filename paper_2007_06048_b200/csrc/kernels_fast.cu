@@ -157,7 +157,8 @@ public:
         cv_in_ = field_map(lay, cv, IC::TX, IC::TY);
         cv_bd_ = field_map(lay, cv, BC::TX, BC::TY);
         const char* ord = std::getenv("MM_FAST_ORDER");
-        order_ = ord && ord[0] == '0' ? 0 : 1;
+        // MM_FAST_ORDER: 2 (default) bit-exact reference order, 1 FMA, 0 factored
+        order_ = ord ? std::max(0, std::min(2, std::atoi(ord))) : 2;
         const char* conc = std::getenv("MM_CONCURRENT");
         concurrent_ = conc && conc[0] == '1';
         cudaDeviceProp prop;
@@ -167,14 +168,18 @@ public:
                                      (int)IC::SMEM));
         MM_CUDA(cudaFuncSetAttribute(k_inner<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)IC::SMEM));
+        MM_CUDA(cudaFuncSetAttribute(k_inner<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)IC::SMEM));
         int per_sm = 0;
         MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inner<R, 1>, IC::NT,
                                                               IC::SMEM));
         inner_per_sm_ = std::max(1, per_sm);
         if constexpr (kBnd) {
-            MM_CUDA(cudaFuncSetAttribute(k_bnd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            MM_CUDA(cudaFuncSetAttribute(k_bnd<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)BC::SMEM));
-            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bnd<R>, BC::NT,
+            MM_CUDA(cudaFuncSetAttribute(k_bnd<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)BC::SMEM));
+            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bnd<R, 2>, BC::NT,
                                                                   BC::SMEM));
             bnd_per_sm_ = std::max(1, per_sm);
         }
@@ -404,7 +409,9 @@ private:
         }
         ip.center = -2.0f * sum;
         const int bc = buf_index(p.pc), bp = buf_index(p.pp);
-        if (order_ == 1)
+        if (order_ == 2)
+            k_inner<R, 2><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
+        else if (order_ == 1)
             k_inner<R, 1><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
         else
             k_inner<R, 0><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
@@ -463,7 +470,10 @@ private:
             bp_.pn = p.pn;
             bp_.segs = w.segs.ptr;
             bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
-            k_bnd<R><<<w.ctas, BC::NT, BC::SMEM, s>>>(maps_, bp_);
+            if (order_ == 2)
+                k_bnd<R, 2><<<w.ctas, BC::NT, BC::SMEM, s>>>(maps_, bp_);
+            else
+                k_bnd<R, 1><<<w.ctas, BC::NT, BC::SMEM, s>>>(maps_, bp_);
             note_launches(1);
             MM_CUDA(cudaGetLastError());
         }
@@ -509,7 +519,10 @@ private:
             }
             auto& e = it->second;
             if (e.count == 0) return;
-            k_pass1<R><<<e.count, 256, 0, s>>>(p, e.runs.ptr, e.items.ptr, e.count);
+            if (order_ == 2)
+                k_pass1<R, 2><<<e.count, 256, 0, s>>>(p, e.runs.ptr, e.items.ptr, e.count);
+            else
+                k_pass1<R, 1><<<e.count, 256, 0, s>>>(p, e.runs.ptr, e.items.ptr, e.count);
             note_launches(1);
             MM_CUDA(cudaGetLastError());
         }
@@ -524,7 +537,7 @@ private:
     Layout lay_;
     int device_;
     int sms_ = 148, inner_per_sm_ = 1, bnd_per_sm_ = 1;
-    int order_ = 1;
+    int order_ = 2;
     bool concurrent_ = false;  // MM_CONCURRENT=1: interior on a side stream, SMs split
     const float* bufs_[3];
     CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;

@@ -71,6 +71,19 @@ def test_fast_engine_within_tolerance_vs_reference_golden(mm, name):
     assert rel_l2(surf, g["surface"]) <= FAST_REL_L2
 
 
+@pytest.mark.parametrize("name", ENGINE_CASES)
+def test_fast_engine_bitwise_vs_reference_golden(mm, name):
+    """The default fast kernels keep the reference's association order with
+    every operation separately rounded: bit-identical, like the strict path."""
+    import os
+    if os.environ.get("MM_FAST_ORDER", "2") != "2":
+        pytest.skip("fast kernels built for a reassociated order")
+    g, e, surf = run_golden(mm, name, "fast")
+    assert np.array_equal(e.pressure(), g["p_cur"])
+    assert np.array_equal(e.pressure_prev(), g["p_prev"])
+    assert np.array_equal(surf, g["surface"])
+
+
 @pytest.mark.parametrize("mode", ["strict", "fast"])
 def test_degenerate_cpml_equals_plain(mm, mode):
     """test_cpml.cpp:134-177 through set_profile."""
