@@ -78,22 +78,19 @@ def byte_model(n, nd, r=4):
     return 16.0 * N + 16.0 * damped, N, damped
 
 
-def update_kernel_bytes(n, nd):
-    """Algorithmic bytes of one launch of the fused update kernel: p_cur,
-    p_prev, c read + p_next write (16 B/pt) + per damped-axis point psi read
-    and zeta read+write (12 B)."""
+def kernel_bytes(n, nd):
+    """Algorithmic bytes per launch of the three step kernels:
+      inner    16 B per inner-box point (p_cur, p_prev, c read; p_next write)
+      boundary 16 B per slab point + 12 B per damped-axis point (psi read,
+               zeta read + write)
+      pass1    8 B per damped-axis point (psi read + write) + 4 B per slab
+               point (p_cur read)"""
     N = float(n[0]) * n[1] * n[2]
     damped = sum(N * 2 * nd[a] / n[a] for a in range(3))
-    return 16.0 * N + 12.0 * damped
-
-
-def pass1_kernel_bytes(n, nd):
-    """pass 1: per damped-axis point psi read+write (8 B) + p_cur read once
-    per damped point (4 B)."""
-    N = float(n[0]) * n[1] * n[2]
-    damped = sum(N * 2 * nd[a] / n[a] for a in range(3))
-    inner = np.prod([n[a] - 2 * nd[a] for a in range(3)])
-    return 8.0 * damped + 4.0 * (N - inner)
+    inner = float(np.prod([n[a] - 2 * nd[a] for a in range(3)]))
+    slab = N - inner
+    return {"inner": 16.0 * inner, "boundary": 16.0 * slab + 12.0 * damped,
+            "pass1": 8.0 * damped + 4.0 * slab}
 
 
 # ------------------------------------------------------------------ clocks
@@ -158,14 +155,15 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload):
-    """dram bytes per launch of the update kernel from the committed ncu summary."""
+def ncu_traffic(workload, kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu
+    summary (profiles/ncu_summary.json, one `ncu --set full` capture)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get(workload, {}).get("update_dram_bytes_per_launch")
+        return d.get(workload, {}).get(kernel, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -247,21 +245,24 @@ def run_ours(args):
     pts = float(n[0]) * n[1] * n[2]
     value = pts * args.steps / (ms * 1e-3) / 1e9
 
-    # per-kernel durations (dominant kernel = the fused update) over K steps
-    k_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # per-kernel durations over K steps, in the step's own order (pass 1,
+    # boundary, interior), CUDA events on the engine's stream
+    k_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     for s in range(args.steps):
         ev = k_ev[s]
         ev[0].record(ext)
         eng.update_boundary_psi()
         ev[1].record(ext)
-        eng.update_planes(0, n[2])
+        eng.update_boundary()
         ev[2].record(ext)
+        eng.update_inner()
+        ev[3].record(ext)
         eng.inject_source(float(w[s % total]), src)
         eng.rotate()
-        ev[3].record(ext)
+        ev[4].record(ext)
     torch.cuda.synchronize()
-    pass1_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in k_ev)
-    upd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in k_ev)
+    kms = {k: statistics.mean(e[i].elapsed_time(e[i + 1]) for e in k_ev)
+           for i, k in enumerate(("pass1", "boundary", "inner"))}
 
     # e2e through the public API with host buffers
     eng2 = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp,
@@ -291,11 +292,14 @@ def run_ours(args):
     e2e = pts * args.steps / (e2e_ms * 1e-3) / 1e9
 
     peak, peak_src = measured_peak()
-    upd_bytes = update_kernel_bytes(n, nd)
-    achieved = upd_bytes / (upd_ms * 1e-3) / 1e9
+    kb = kernel_bytes(n, nd)
+    dominant = max(kms, key=kms.get)
+    achieved = kb[dominant] / (kms[dominant] * 1e-3) / 1e9
     step_bytes, _, _ = byte_model(n, nd)
     step_gbs = step_bytes * args.steps / (ms * 1e-3) / 1e9
-    traffic = ncu_traffic(f"{edge}^3")
+    traffic = ncu_traffic(f"{edge}^3", dominant)
+    per_kernel = {k: {"ms": round(kms[k], 4), "algorithmic_bytes": kb[k],
+                      "achieved_gbs": round(kb[k] / (kms[k] * 1e-3) / 1e9, 1)} for k in kms}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
@@ -311,14 +315,14 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "kernel": "update (inner + CPML pass 2)",
-                     "algorithmic_bytes_per_launch": upd_bytes,
-                     "kernel_ms": round(upd_ms, 4), "peak_source": peak_src},
+                     "traffic": traffic, "kernel": dominant,
+                     "algorithmic_bytes_per_launch": kb[dominant],
+                     "kernel_ms": round(kms[dominant], 4), "peak_source": peak_src},
+        "kernels": per_kernel,
         "step_roofline": {"bytes_per_step_model": step_bytes,
                           "achieved_gbs": round(step_gbs, 1),
                           "frac": round(step_gbs / peak, 4),
-                          "roofline_gpts": round(peak * 1e9 / (step_bytes / pts) / 1e9, 1),
-                          "pass1_ms": round(pass1_ms, 4), "update_ms": round(upd_ms, 4)},
+                          "roofline_gpts": round(peak * 1e9 / (step_bytes / pts) / 1e9, 1)},
         "clocks": clk,
     }
     if not args.no_cpu_baseline:
