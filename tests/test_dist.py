@@ -1,0 +1,141 @@
+"""Z-slab decomposition host logic (paper_2007_06048_b200.dist).
+
+CPU tests: decomposition arithmetic (ref: test_dist.cpp:32-41), the legality
+rule (dist.cpp:119-132), cost-weighted cuts, and a world_size-2 gloo run of
+the halo-exchange plan driving the CPU oracle engines, bit-identical to the
+single-rank run (test_dist.cpp:107-118 restated for z cuts)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2007_06048_b200 import dist as D
+from paper_2007_06048_b200._lib import ConfigError
+
+
+def test_decompose_matches_reference():
+    assert [D.decompose(100, 3, c) for c in range(3)] == [(0, 34), (34, 33), (67, 33)]
+    assert D.decompose(1024, 4, 3) == (768, 256)
+    assert D.decompose(7, 1, 0) == (0, 7)
+    with pytest.raises(ConfigError):
+        D.decompose(3, 4, 0)
+
+
+def test_cuts_through_damping_are_rejected():
+    # test_dist.cpp:120-127: 32 points, nd 8, r 4, 4 parts -> cuts 8/16/24 illegal
+    with pytest.raises(ConfigError, match="damping"):
+        D.validate_cuts(D.equal_cuts(32, 4), 32, 8, 4)
+    D.validate_cuts(D.equal_cuts(64, 2), 64, 8, 4)
+
+
+@pytest.mark.parametrize("n,parts", [(1000, 8), (512, 8), (1000, 4), (512, 2), (240, 2)])
+def test_weighted_cuts_are_legal_and_balanced(n, parts):
+    nd = (27, 27, 27)
+    cuts = D.weighted_cuts((n, n, n), nd, 4, parts)
+    assert cuts[0] == 0 and cuts[-1] == n and len(cuts) == parts + 1
+    D.validate_cuts(cuts, n, 27, 4)
+    assert D.balance((n, n, n), nd, cuts) >= 0.98
+    # equal cuts leave the CPML end slabs overloaded (SURVEY finding 6)
+    if (n, parts) == (1000, 8):
+        assert abs(D.balance((n, n, n), nd, D.equal_cuts(n, parts)) - 0.878) < 0.01
+
+
+def test_weighted_cuts_reject_impossible_layouts():
+    # 100^3 at 4 ranks: the reference's equal cuts (25/50/75) are illegal, the
+    # weighted cuts stay inside [31, 69]
+    cuts = D.weighted_cuts((100, 100, 100), (27, 27, 27), 4, 4)
+    assert all(31 <= c <= 69 for c in cuts[1:-1])
+    with pytest.raises(ConfigError):
+        D.validate_cuts(D.equal_cuts(100, 4), 100, 27, 4)
+    with pytest.raises(ConfigError):
+        D.weighted_cuts((60, 60, 60), (27, 27, 27), 4, 2)  # no legal cut exists
+
+
+def test_halo_plan():
+    info = D.SlabInfo(1, 3, [0, 10, 20, 30])
+    assert (info.z0, info.nz, info.lower, info.upper) == (10, 10, 0, 2)
+    assert D.halo_pairs(info) == [(0, 0), (2, 1)]
+    assert D.halo_pairs(D.SlabInfo(0, 1, [0, 30])) == []
+
+
+# ------------------------------------------------------------ gloo, world 2
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, n, nd, steps, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_2007_06048_b200 import dist as D
+        o = Oracle("port")
+        r = 4
+        vp, vmin, vmax = o.layered_model(n)
+        cuts = D.weighted_cuts(n, nd, r, world)
+        info = D.SlabInfo(rank, world, cuts)
+        eng = o.engine((n[0], n[1], info.nz), D.local_vp(vp, r, info.z0, info.nz),
+                       offset=(0, 0, info.z0), global_n=n, ndamping=nd, taper=True,
+                       ntaper=(2, 2, 2), dt=1.61e-3, vmax=vmax)
+        w = o.ricker(25.0, 1.61e-3, steps)
+        src = (n[0] // 2, n[1] // 2, n[2] // 2)
+        src_local = (src[0], src[1], src[2] - info.z0) if info.z0 <= src[2] < info.z0 + info.nz \
+            else None
+        tr = D.TorchTransport()
+        for s in range(steps):
+            # exchange_halos(p_cur) then step (dist.cpp:213-215), planes packed
+            # into contiguous tensors (the CPU field is z-fastest)
+            pc, pp = eng.pressure(), eng.pressure_prev()
+            sends, recvs = [], []
+            for peer, side in D.halo_pairs(info):
+                own = pc[:, :, r:2 * r] if side == 0 else pc[:, :, -2 * r:-r]
+                sends.append((peer, torch.from_numpy(np.ascontiguousarray(own))))
+                recvs.append((peer, torch.empty(own.shape, dtype=torch.float32)))
+            tr.wait(tr.exchange(sends, recvs))
+            for (peer, side), (_, buf) in zip(D.halo_pairs(info), recvs):
+                if side == 0:
+                    pc[:, :, :r] = buf.numpy()
+                else:
+                    pc[:, :, -r:] = buf.numpy()
+            eng.set_state(pp, pc)
+            eng.step(float(w[s]), src_local)
+        q.put((rank, info.z0, info.nz, eng.pressure()[:, :, r:-r].copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_zslab_equals_single_rank():
+    import torch.multiprocessing as mp
+    from oracle.oracle import Oracle
+    n, nd, steps = (24, 24, 48), (4, 4, 4), 30
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, n, nd, steps, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    o = Oracle("port")
+    vp, _, vmax = o.layered_model(n)
+    whole = o.engine(n, vp, ndamping=nd, taper=True, ntaper=(2, 2, 2), dt=1.61e-3, vmax=vmax)
+    w = o.ricker(25.0, 1.61e-3, steps)
+    for s in range(steps):
+        whole.step(float(w[s]), (n[0] // 2, n[1] // 2, n[2] // 2))
+    full = whole.pressure()[:, :, 4:-4]
+    covered = 0
+    for rank, z0, nz, field in sorted(parts):
+        assert np.array_equal(field[4:-4, 4:-4], full[4:-4, 4:-4, z0:z0 + nz]), rank
+        covered += nz
+    assert covered == n[2]
