@@ -10,7 +10,10 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libminimod_b200.so"
+# MM_LIB_VARIANT=<name> loads an experiment build (build.py --variant <name>)
+LIB_PATH = Path(__file__).resolve().parent / (
+    f"libminimod_b200_{os.environ['MM_LIB_VARIANT']}.so" if os.environ.get("MM_LIB_VARIANT")
+    else "libminimod_b200.so")
 
 MM_OK, MM_ECONFIG, MM_EVALIDATION, MM_EINSTABILITY, MM_EINVAL, MM_ECUDA, MM_ENCCL = range(7)
 MM_MODE_FAST, MM_MODE_STRICT = 0, 1

@@ -51,12 +51,13 @@ def _headers_mtime() -> float:
     return max((h.stat().st_mtime for h in hs), default=0.0)
 
 
-def _compile(src: Path, force: bool) -> Path:
-    obj = BUILD / (src.name + ".o")
+def _compile(src: Path, force: bool, bdir: Path = BUILD, defines=()) -> Path:
+    obj = bdir / (src.name + ".o")
     if (not force and obj.exists() and obj.stat().st_mtime >= src.stat().st_mtime
             and obj.stat().st_mtime >= _headers_mtime()):
         return obj
-    cmd = [nvcc(), *ARCH, *COMMON, *EXTRA.get(src.name, []), "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *ARCH, *COMMON, *EXTRA.get(src.name, []), *[f"-D{d}" for d in defines],
+           "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
@@ -65,23 +66,33 @@ def _compile(src: Path, force: bool) -> Path:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    BUILD.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> Path:
+    """Build the library.  `variant` + `defines` build an experiment copy
+    (libminimod_b200_<variant>.so, loaded when MM_LIB_VARIANT=<variant>)."""
+    bdir = BUILD.with_name(BUILD.name + (f"_{variant}" if variant else ""))
+    lib = LIB.with_name(f"libminimod_b200_{variant}.so") if variant else LIB
+    bdir.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), srcs))
+        objs = list(ex.map(lambda s: _compile(s, force, bdir, defines), srcs))
     newest = max(o.stat().st_mtime for o in objs)
-    if force or not LIB.exists() or LIB.stat().st_mtime < newest:
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or not lib.exists() or lib.stat().st_mtime < newest:
+        tmp = lib.with_suffix(".so.tmp")
         cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
-        os.replace(tmp, LIB)
+        os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {lib}")
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    a = ap.parse_args()
+    build(force=a.force, verbose=True, variant=a.variant, defines=a.defines)

@@ -1,0 +1,346 @@
+// fast_pass1.cuh -- CPML pass 1, MM_MODE_FAST.
+//
+// ref: update_damping_pass1 (propagator_impl.hpp:106-123):
+//        psi_a = b_a * psi_a + a_a * D1_a(p_cur)   over every damping run.
+//
+// k_p1: a persistent, warp-specialised TMA stream.  One work item is a run x a
+// 32 x 16 x-y tile x a z chunk.  The producer lane streams, per plane, the
+// p_cur box the axis' first derivative needs (x halo for x runs, y halo for y
+// runs, a 2R+1-plane ring for z runs) and the psi tile into shared memory;
+// four consumer warps (one float4 of x points per thread) compute the new psi
+// and store it with coalesced 16-byte global stores.  Bytes in flight are held
+// by TMA, not registers, so the kernel streams at HBM rate.
+#pragma once
+
+#include "fast_common.cuh"
+
+namespace mmb {
+namespace fast {
+
+#ifndef MM_P1_LEAD
+#define MM_P1_LEAD 4
+#endif
+
+template <int R>
+struct P1Cfg {
+    static constexpr int TX = 32, TY = 16;
+    static constexpr int NC = (TX / 4) * TY;  // 128 consumer threads, float4 each
+    static constexpr int NCW = NC / 32;
+    static constexpr int NT = NC + 32;        // + producer warp
+    static constexpr int HX = R <= 4 ? 4 : 8;  // x halo (16-byte aligned TMA starts)
+    static constexpr int BXX = TX + 2 * HX;    // x-run p box width
+    static constexpr int BYY = TY + 2 * R;     // y-run p box height
+    static constexpr int PXN = BXX * TY, PYN = TX * BYY, PZN = TX * TY;
+    static constexpr int PSLOT = pad32(PXN > PYN ? PXN : PYN);
+    static constexpr int PSI_N = TX * TY, PSI = pad32(PSI_N);
+    static constexpr int D = MM_P1_LEAD;      // producer lead beyond the z window
+    static constexpr int NS = 2 * R + 1 + D;  // p slots
+    static constexpr int NQ = MM_P1_LEAD;     // psi stages
+    static constexpr int QLEAD = NQ - 1;
+    static constexpr int QW = 2 * R + 1;      // window of new psi_z planes
+    static constexpr int NBAR = 2 * NS + 2 * NQ + 4;
+    static constexpr size_t SMEM =
+        sizeof(float) * (size_t)(NS * PSLOT + NQ * PSI + QW * PSI) + 8 * NBAR + 64;
+};
+
+struct P1Maps {
+    CUtensorMap px, py, pz;  // p_cur: x-run box, y-run box, plain tile
+    CUtensorMap psi[3][2];
+};
+
+// One damping run as a box of points (local coordinates).
+struct RunDesc {
+    int ax, side;
+    int lo[3], hi[3];
+    int x_base;  // multiple of 4 (the run array origin for axis 0)
+};
+
+struct P1Params {
+    Layout lay;
+    RunDesc rd[6];
+    CpmlRun run[3][2];
+    const float* ta[3];
+    const float* tb[3];
+    float c1[3][kMaxR];
+    const int4* items;  // (run | tile_x << 3, tile_y, z_begin, z_end)
+    WorkQueue wq;
+    // dpsi_z = D1_z(new psi_z) of each z run over its planes lo-R .. hi+R-1,
+    // same x/y strides as the run's psi array (plane index z - (lo - R)).
+    float* dpz[2];
+};
+
+template <int R>
+struct P1Tile {
+    int ax, side, x0, y0, zb, ze, w, nring, nout;
+    __device__ P1Tile(const P1Params& P, const int4& sg) {
+        const RunDesc& d = P.rd[sg.x & 7];
+        ax = d.ax;
+        side = d.side;
+        x0 = d.x_base + (sg.x >> 3) * P1Cfg<R>::TX;
+        y0 = d.lo[1] + sg.y * P1Cfg<R>::TY;
+        zb = sg.z;
+        ze = sg.w;
+        w = ax == 2 ? R : 0;  // z window half-width
+        nout = ze - zb;
+        nring = nout + 2 * w;
+    }
+};
+
+template <int R, int ORD>
+__global__ void __launch_bounds__(P1Cfg<R>::NT)
+    k_p1(const __grid_constant__ P1Maps M, const P1Params P) {
+    using C = P1Cfg<R>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    float* qring = ring + C::NS * C::PSLOT;
+    float* zwin = qring + C::NQ * C::PSI;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(zwin + C::QW * C::PSI);
+    int4* items = reinterpret_cast<int4*>(bars + C::NBAR);
+    const uint32_t fullP = smem_u32(bars), emptyP = fullP + 8 * C::NS;
+    const uint32_t fullQ = emptyP + 8 * C::NS, emptyQ = fullQ + 8 * C::NQ;
+    const uint32_t fullI = emptyQ + 8 * C::NQ, emptyI = fullI + 16;
+    const int tid = threadIdx.x;
+    const int warp = tid / 32, lane = tid % 32;
+    const Layout L = P.lay;
+
+    if (tid == 0) {
+        for (int s = 0; s < C::NS; ++s) {
+            mbar_init(fullP + 8 * s, 1);
+            mbar_init(emptyP + 8 * s, C::NCW);
+        }
+        for (int s = 0; s < C::NQ; ++s) {
+            mbar_init(fullQ + 8 * s, 1);
+            mbar_init(emptyQ + 8 * s, C::NCW);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(fullI + 8 * s, 1);
+            mbar_init(emptyI + 8 * s, C::NCW);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == C::NCW) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            unsigned np = 0, nq = 0, ni = 0;
+            for (;;) {
+                const int item = atomicAdd(P.wq.ctr, 1);
+                const int4 sg = item < P.wq.nitems ? P.items[item] : make_int4(0, 0, 0, -1);
+                {
+                    const int s = ni & 1;
+                    mbar_wait_sleep(emptyI + 8 * s, ((ni >> 1) & 1) ^ 1);
+                    items[s] = sg;
+                    mbar_arrive_b(fullI + 8 * s);
+                    ++ni;
+                }
+                if (sg.w < 0) break;
+                const P1Tile<R> T(P, sg);
+                const CpmlRun& run = P.run[T.ax][T.side];
+                const CUtensorMap* pmap = T.ax == 0 ? &M.px : T.ax == 1 ? &M.py : &M.pz;
+                const uint32_t pbytes = 4u * (T.ax == 0 ? C::PXN : T.ax == 1 ? C::PYN : C::PZN);
+                const int px = L.L + T.x0 - (T.ax == 0 ? C::HX : 0);
+                const int py = T.y0 + L.r - (T.ax == 1 ? R : 0);
+                // psi tile origin in the run array (run_off's coordinates)
+                const int qx = T.x0 - (T.ax == 0 ? run.org : 0);
+                const int qy = T.y0 - (T.ax == 1 ? run.org : 0);
+                const int qz = T.ax == 2 ? run.org : 0;
+                auto issue_q = [&](int o) {
+                    const int s = nq % C::NQ;
+                    mbar_wait_sleep(emptyQ + 8 * s, ((nq / C::NQ) & 1) ^ 1);
+                    const uint32_t bar = fullQ + 8 * s;
+                    mbar_expect_tx(bar, 4u * C::PSI_N);
+                    tma_load_3d(smem_u32(qring + s * C::PSI), &M.psi[T.ax][T.side], qx, qy,
+                                T.zb + o - qz, bar);
+                    ++nq;
+                };
+                int oq = 0;
+                for (int j = 0; j < T.nring; ++j) {
+                    const int z = T.zb - T.w + j;
+                    const int s = np % C::NS;
+                    mbar_wait_sleep(emptyP + 8 * s, ((np / C::NS) & 1) ^ 1);
+                    const uint32_t bar = fullP + 8 * s;
+                    mbar_expect_tx(bar, pbytes);
+                    tma_load_3d(smem_u32(ring + s * C::PSLOT), pmap, px, py, z + L.r, bar);
+                    ++np;
+                    for (; oq < T.nout && oq <= j - 2 * T.w + C::QLEAD; ++oq) issue_q(oq);
+                }
+                for (; oq < T.nout; ++oq) issue_q(oq);
+            }
+            __threadfence();
+            if (atomicAdd(P.wq.ctr + 1, 1) == (int)gridDim.x - 1) {
+                atomicExch(P.wq.ctr, 0);
+                atomicExch(P.wq.ctr + 1, 0);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int tx = tid % (C::TX / 4), ty = tid / (C::TX / 4);
+    unsigned np = 0, nq = 0, ni = 0;
+    for (;;) {
+        int4 sg;
+        {
+            const int s = ni & 1;
+            mbar_wait(fullI + 8 * s, (ni >> 1) & 1);
+            sg = items[s];
+            __syncwarp();
+            if (lane == 0) mbar_arrive_b(emptyI + 8 * s);
+            ++ni;
+        }
+        if (sg.w < 0) break;
+        const P1Tile<R> T(P, sg);
+        const int ax = T.ax;
+        const RunDesc& d = P.rd[sg.x & 7];
+        const CpmlRun& run = P.run[ax][T.side];
+        const int x = T.x0 + 4 * tx, y = T.y0 + ty;
+        bool ok[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            ok[e] = x + e >= d.lo[0] && x + e < d.hi[0] && y >= d.lo[1] && y < d.hi[1];
+        const bool all = ok[0] && ok[1] && ok[2] && ok[3];
+        const bool any = ok[0] || ok[1] || ok[2] || ok[3];
+        float c1[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) c1[m] = P.c1[ax][m];
+        // damping coefficients: per x (x runs), per y (y runs), per z (z runs)
+        float av[4], bv[4];
+        if (ax == 0) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int xc = min(max(x + e, 0), L.n[0] - 1);
+                av[e] = __ldg(P.ta[0] + xc);
+                bv[e] = __ldg(P.tb[0] + xc);
+            }
+        } else {
+            const int yc = min(max(y, 0), L.n[1] - 1);
+            const float a = ax == 1 ? __ldg(P.ta[1] + yc) : 0.f;
+            const float b = ax == 1 ? __ldg(P.tb[1] + yc) : 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                av[e] = a;
+                bv[e] = b;
+            }
+        }
+        float* dst = run.psi + run_off(run, ax, x, y, T.zb);
+        const long long zstep = run.s2;
+        // offset of this thread's 4 points in a p slot
+        const int poff = ax == 0 ? ty * C::BXX + C::HX + 4 * tx
+                         : ax == 1 ? (ty + R) * C::TX + 4 * tx
+                                   : ty * C::TX + 4 * tx;
+        const int qoff = ty * C::TX + 4 * tx;
+        auto store4 = [&](float* q, const float4& v) {
+            if (all) {
+                *reinterpret_cast<float4*>(q) = v;
+            } else if (any) {
+                if (ok[0]) q[0] = v.x;
+                if (ok[1]) q[1] = v.y;
+                if (ok[2]) q[2] = v.z;
+                if (ok[3]) q[3] = v.w;
+            }
+        };
+        // z runs (items cover the whole run, zb = lo, ze = hi): dpsi_z at plane
+        // zb + od for od = -R .. nout+R-1, from the new psi_z window
+        auto emit_dpz = [&](int od) {
+            float dz[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int m = 1; m <= R; ++m) {
+                const int a = od + m, b = od - m;
+                const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 u4 = a >= 0 && a < T.nout ? lds4(zwin + (a % C::QW) * C::PSI + qoff) : zero;
+                const float4 d4 = b >= 0 && b < T.nout ? lds4(zwin + (b % C::QW) * C::PSI + qoff) : zero;
+                dz[0] = acc<ORD>(dz[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
+                dz[1] = acc<ORD>(dz[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
+                dz[2] = acc<ORD>(dz[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
+                dz[3] = acc<ORD>(dz[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
+            }
+            store4(P.dpz[T.side] + x + (long long)y * run.s1 + (long long)(od + R) * run.s2,
+                   make_float4(dz[0], dz[1], dz[2], dz[3]));
+        };
+#pragma unroll 1
+        for (int j = 0; j < T.nring; ++j) {
+            const int s = np % C::NS;
+            mbar_wait(fullP + 8 * s, (np / C::NS) & 1);
+            if (j >= 2 * T.w) {
+                const int o = j - 2 * T.w;
+                const int z = T.zb + o;
+                if (ax == 2) {
+                    const float a = __ldg(P.ta[2] + z), b = __ldg(P.tb[2] + z);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        av[e] = a;
+                        bv[e] = b;
+                    }
+                }
+                const int cs = (np + C::NS - T.w) % C::NS;  // slot of plane j - w
+                auto slot_of = [&](int m) {                 // slot of plane j - w + m
+                    const int t = cs + m;
+                    return t < 0 ? t + C::NS : t >= C::NS ? t - C::NS : t;
+                };
+                float dp[4] = {0.f, 0.f, 0.f, 0.f};
+                const float* S = ring + cs * C::PSLOT + poff;
+                if (ax == 0) {
+                    constexpr int H = C::HX;
+                    float v[4 + 2 * H];
+#pragma unroll
+                    for (int h = 0; h < (4 + 2 * H) / 4; ++h) {
+                        const float4 t = lds4(S - H + 4 * h);
+                        v[4 * h] = t.x;
+                        v[4 * h + 1] = t.y;
+                        v[4 * h + 2] = t.z;
+                        v[4 * h + 3] = t.w;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+#pragma unroll
+                        for (int m = 1; m <= R; ++m)
+                            dp[e] = acc<ORD>(dp[e], c1[m - 1], fs<ORD>(v[H + e + m], v[H + e - m]));
+                } else {
+#pragma unroll
+                    for (int m = 1; m <= R; ++m) {
+                        const float4 u4 = ax == 1 ? lds4(S + m * C::TX)
+                                                  : lds4(ring + slot_of(m) * C::PSLOT + poff);
+                        const float4 d4 = ax == 1 ? lds4(S - m * C::TX)
+                                                  : lds4(ring + slot_of(-m) * C::PSLOT + poff);
+                        dp[0] = acc<ORD>(dp[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
+                        dp[1] = acc<ORD>(dp[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
+                        dp[2] = acc<ORD>(dp[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
+                        dp[3] = acc<ORD>(dp[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
+                    }
+                }
+                const int st = nq % C::NQ;
+                mbar_wait(fullQ + 8 * st, (nq / C::NQ) & 1);
+                float4 v = lds4(qring + st * C::PSI + qoff);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_b(emptyQ + 8 * st);
+                ++nq;
+                // reference: psi = b * psi + a * dp  (propagator_impl.hpp:118-120)
+                v.x = acc<ORD>(fm<ORD>(av[0], dp[0]), bv[0], v.x);
+                v.y = acc<ORD>(fm<ORD>(av[1], dp[1]), bv[1], v.y);
+                v.z = acc<ORD>(fm<ORD>(av[2], dp[2]), bv[2], v.z);
+                v.w = acc<ORD>(fm<ORD>(av[3], dp[3]), bv[3], v.w);
+                store4(dst + (long long)o * zstep, v);
+                // plane j - 2w has had its last use
+                __syncwarp();
+                if (lane == 0) mbar_arrive_b(emptyP + 8 * slot_of(-T.w));
+                if (ax == 2) {
+                    // this thread's window of new psi_z (no other thread reads it)
+                    *reinterpret_cast<float4*>(zwin + (o % C::QW) * C::PSI + qoff) = v;
+                    emit_dpz(o - R);  // its window ends at plane o
+                }
+            }
+            ++np;
+        }
+        if (ax == 2)  // planes whose window reaches past the run: psi_z = 0 there
+            for (int od = T.nout - R; od < T.nout + R; ++od) emit_dpz(od);
+#pragma unroll 1
+        for (int k = 2 * T.w; k >= 1; --k) {  // the item's last 2w planes
+            __syncwarp();
+            if (lane == 0) mbar_arrive_b(emptyP + 8 * ((np + C::NS - k) % C::NS));
+        }
+    }
+}
+
+}  // namespace fast
+}  // namespace mmb

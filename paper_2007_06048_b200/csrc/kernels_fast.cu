@@ -5,7 +5,7 @@
 // then the source injection after the join.  The interior and boundary
 // kernels are persistent: their grids split the GPU's CTA slots in
 // proportion to their algorithmic bytes so both finish together.
-// Kernels: fast_inner.cuh (k_inner), fast_boundary.cuh (k_bnd, k_pass1).
+// Kernels: fast_inner.cuh (k_inner), fast_boundary.cuh (k_bnd), fast_pass1.cuh (k_p1).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -18,6 +18,7 @@
 
 #include "fast_boundary.cuh"
 #include "fast_inner.cuh"
+#include "fast_pass1.cuh"
 #include "mm_fast.hpp"
 
 namespace mmb {
@@ -103,6 +104,15 @@ struct DArr {
         MM_CUDA(cudaMemcpyAsync(ptr, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
         MM_CUDA(cudaStreamSynchronize(s));
     }
+    void alloc_zero(size_t count, cudaStream_t s) {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        n = count;
+        if (n == 0) return;
+        MM_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+        MM_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));
+        MM_CUDA(cudaStreamSynchronize(s));
+    }
 };
 
 struct Box {
@@ -113,12 +123,13 @@ struct Box {
 // Items are ordered chunk-major (all tiles of chunk 0, then chunk 1, ...) and
 // handed out dynamically (WorkQueue), so the items in flight at any moment are
 // neighbouring tiles at the same z and their halo planes meet in L2.  The
-// chunk length is chosen so that every CTA gets about one or more waves of
-// ~48-plane items.
+// chunk length is chosen so that every CTA gets about per_cta / target
+// items (at least one), `target` planes long.
 struct Item {
     int tag, ty, zlo, zhi;
 };
-void wave_items(const std::vector<Item>& tiles, int ctas, std::vector<int4>& out) {
+void wave_items(const std::vector<Item>& tiles, int ctas, double target,
+                std::vector<int4>& out) {
     out.clear();
     if (tiles.empty()) return;
     long long tp = 0;
@@ -128,7 +139,7 @@ void wave_items(const std::vector<Item>& tiles, int ctas, std::vector<int4>& out
         zmax = std::max(zmax, t.zhi - t.zlo);
     }
     const double per_cta = (double)tp / std::max(1, ctas);
-    const int waves = std::max(1, (int)std::lround(per_cta / 48.0));
+    const int waves = std::max(1, (int)std::lround(per_cta / target));
     const int zc = std::max(4, (int)((tp + (long long)ctas * waves - 1) / ((long long)ctas * waves)));
     for (int k = 0; (long long)k * zc < zmax; ++k)
         for (const auto& t : tiles) {
@@ -142,7 +153,9 @@ template <int R>
 class FastPlanR final : public FastPlan {
     using IC = InnerCfg<R>;
     using BC = BndCfg<R>;
-    static constexpr bool kBnd = BC::SMEM <= 200 * 1024;  // TMA boundary kernel fits
+    using P1C = P1Cfg<R>;
+    static constexpr bool kBnd = R <= 4;  // TMA boundary kernel (R = 8: strict kernels)
+    static constexpr bool kP1 = P1C::SMEM <= 200 * 1024;
 
 public:
     FastPlanR(const Layout& lay, int device, float* const bufs[3], const float* cv)
@@ -153,12 +166,23 @@ public:
             in_tile_[b] = field_map(lay, bufs[b], IC::TX, IC::TY);
             bd_halo_[b] = field_map(lay, bufs[b], BC::BX, BC::BY);
             bd_tile_[b] = field_map(lay, bufs[b], BC::TX, BC::TY);
+            p1x_[b] = field_map(lay, bufs[b], P1C::BXX, P1C::TY);
+            p1y_[b] = field_map(lay, bufs[b], P1C::TX, P1C::BYY);
+            p1z_[b] = field_map(lay, bufs[b], P1C::TX, P1C::TY);
         }
         cv_in_ = field_map(lay, cv, IC::TX, IC::TY);
         cv_bd_ = field_map(lay, cv, BC::TX, BC::TY);
         const char* ord = std::getenv("MM_FAST_ORDER");
         // MM_FAST_ORDER: 2 (default) bit-exact reference order, 1 FMA, 0 factored
         order_ = ord ? std::max(0, std::min(2, std::atoi(ord))) : 2;
+        // z-chunk targets (planes per work item) of the two persistent kernels
+        auto envf = [](const char* k, double d) {
+            const char* v = std::getenv(k);
+            return v ? std::max(1.0, std::atof(v)) : d;
+        };
+        inner_zt_ = envf("MM_INNER_ZT", 48.0);
+        bnd_zt_ = envf("MM_BND_ZT", 24.0);
+        p1_zt_ = envf("MM_P1_ZT", 16.0);
         const char* conc = std::getenv("MM_CONCURRENT");
         concurrent_ = conc && conc[0] == '1';
         cudaDeviceProp prop;
@@ -182,6 +206,15 @@ public:
             MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bnd<R, 2>, BC::NT,
                                                                   BC::SMEM));
             bnd_per_sm_ = std::max(1, per_sm);
+        }
+        if constexpr (kP1) {
+            MM_CUDA(cudaFuncSetAttribute(k_p1<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)P1C::SMEM));
+            MM_CUDA(cudaFuncSetAttribute(k_p1<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)P1C::SMEM));
+            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p1<R, 2>, P1C::NT,
+                                                                  P1C::SMEM));
+            p1_per_sm_ = std::max(1, per_sm);
         }
         MM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
         MM_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
@@ -313,9 +346,9 @@ private:
         return ((long long)z_lo << 32) ^ ((long long)z_hi << 1) ^ (conc ? 1 : 0);
     }
 
-    void finish_work(Work& w, const std::vector<Item>& tiles, int ctas) {
+    void finish_work(Work& w, const std::vector<Item>& tiles, int ctas, double target) {
         std::vector<int4> items;
-        wave_items(tiles, ctas, items);
+        wave_items(tiles, ctas, target, items);
         w.nitems = (int)items.size();
         w.ctas = std::max(1, std::min(ctas, w.nitems));
         w.segs.set(items, stream_setup_);
@@ -345,7 +378,7 @@ private:
                 tiles.push_back(Item{tx, ty, inner.lo[2], inner.hi[2]});
         int gi, gb;
         budgets(p, z_lo, z_hi, conc, gi, gb);
-        finish_work(w, tiles, std::max(1, gi));
+        finish_work(w, tiles, std::max(1, gi), inner_zt_);
         return w;
     }
 
@@ -359,7 +392,13 @@ private:
         regions(p, inner, slabs);
         std::vector<Item> items;  // one per tile
         w.nbox = 0;
+        // MM_BND_KINDS (profiling only): bit mask of the slab kinds to update
+        static const int kinds = [] {
+            const char* e = std::getenv("MM_BND_KINDS");
+            return e ? std::atoi(e) : 7;
+        }();
         for (const auto& s : slabs) {
+            if (!((kinds >> (s.first / 2)) & 1)) continue;
             const Box& b = s.second;
             const int zl = std::max(b.lo[2], z_lo), zh = std::min(b.hi[2], z_hi);
             if (zh <= zl) continue;
@@ -382,7 +421,7 @@ private:
         w.empty = false;
         int gi, gb;
         budgets(p, z_lo, z_hi, conc, gi, gb);
-        finish_work(w, items, std::max(1, gb));
+        finish_work(w, items, std::max(1, gb), bnd_zt_);
         return w;
     }
 
@@ -419,6 +458,31 @@ private:
         MM_CUDA(cudaGetLastError());
     }
 
+    // dpsi_z planes [lo-R, hi+R) of each z run (k_p1 writes, k_bnd reads).  When
+    // the two ranges would overlap (z extent < 2 (nd + R)), a plane's dpsi_z mixes
+    // both runs and the strict kernels do pass 1 and the slabs instead.
+    bool ensure_dpz(const StepParams& p) {
+        if (dpz_valid_) return !zmix_;
+        const CpmlRun& r0 = p.run[2][0];
+        const CpmlRun& r1 = p.run[2][1];
+        const bool h0 = r0.hi > r0.lo, h1 = r1.hi > r1.lo;
+        zmix_ = h0 && h1 && r0.hi + R > r1.lo - R;
+        for (int sd = 0; sd < 2; ++sd) {
+            const CpmlRun& r = p.run[2][sd];
+            dz_lo_[sd] = 0;
+            dz_hi_[sd] = 0;
+            if (r.hi <= r.lo || zmix_) continue;
+            dz_lo_[sd] = r.lo - R;
+            dz_hi_[sd] = r.hi + R;
+            const long long planes = r.hi - r.lo + 2 * R;
+            dpz_[sd].alloc_zero((size_t)(r.s2 * planes), stream_setup_);
+            maps_.dpz[sd] = make_map(dpz_[sd].ptr, r.s1, lay_.n[1], planes, r.s1, r.s2, BC::TX,
+                                     BC::TY);
+        }
+        dpz_valid_ = true;
+        return !zmix_;
+    }
+
     void refresh_run_maps(const StepParams& p) {
         bool same = true;
         for (int a = 0; a < 3; ++a)
@@ -435,15 +499,20 @@ private:
                 if (a == 1) by = BC::BY;  // y halo
                 maps_.psi[a][sd] = run_map(lay_, r, a, r.psi, bx, by);
                 maps_.zeta[a][sd] = run_map(lay_, r, a, r.zeta, BC::TX, BC::TY);
+                p1maps_.psi[a][sd] = run_map(lay_, r, a, r.psi, P1C::TX, P1C::TY);
             }
         runs_valid_ = true;
     }
 
     void launch_boundary(const StepParams& p, int z_lo, int z_hi, bool conc, cudaStream_t s) {
-        if constexpr (!kBnd) {
+        if constexpr (!(kBnd && kP1)) {
             strict_update(p, 2, z_lo, z_hi, s);
             return;
         } else {
+            if (!ensure_dpz(p)) {
+                strict_update(p, 2, z_lo, z_hi, s);
+                return;
+            }
             Work& w = bnd_work(p, z_lo, z_hi, conc);
             if (w.empty) return;
             refresh_run_maps(p);
@@ -467,6 +536,10 @@ private:
                     bp_.c1[a][m] = p.c1[a][m];
                 }
             }
+            for (int sd = 0; sd < 2; ++sd) {
+                bp_.dz_lo[sd] = dz_lo_[sd];
+                bp_.dz_hi[sd] = dz_hi_[sd];
+            }
             bp_.pn = p.pn;
             bp_.segs = w.segs.ptr;
             bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
@@ -480,15 +553,20 @@ private:
     }
 
     void launch_pass1(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) {
-        if constexpr (!kBnd) {
+        if constexpr (!(kBnd && kP1)) {
             strict_pass1(p, z_lo, z_hi, s);
             return;
         } else {
+            if (!ensure_dpz(p)) {
+                strict_pass1(p, z_lo, z_hi, s);
+                return;
+            }
             const auto key = std::make_pair(z_lo, z_hi);
             auto it = pass1_cache_.find(key);
             if (it == pass1_cache_.end()) {
-                std::vector<RunDesc> runs;
-                std::vector<int4> items;
+                Pass1Work& e = pass1_cache_[key];
+                std::vector<Item> tiles;
+                std::vector<int4> zitems;
                 for (int ax = 0; ax < 3; ++ax)
                     for (int side = 0; side < 2; ++side) {
                         const CpmlRun& r = p.run[ax][side];
@@ -499,39 +577,69 @@ private:
                         d.lo[2] = std::max(d.lo[2], z_lo);
                         d.hi[2] = std::min(d.hi[2], z_hi);
                         if (d.hi[2] <= d.lo[2]) continue;
-                        d.x_base = d.lo[0] & ~3;
-                        const int ri = (int)runs.size();
-                        runs.push_back(d);
-                        const int tx = (d.hi[0] - d.x_base + 31) / 32;
-                        const int ty = (d.hi[1] - d.lo[1] + 31) / 32;
-                        const int zc = ax == 2 ? d.hi[2] - d.lo[2] : 16;
-                        for (int zb = d.lo[2]; zb < d.hi[2]; zb += zc)
-                            for (int b = 0; b < ty; ++b)
-                                for (int a = 0; a < tx; ++a)
-                                    items.push_back(make_int4(ri | (a << 4), b, zb,
-                                                              std::min(d.hi[2], zb + zc)));
+                        d.x_base = d.lo[0] & ~3;  // = r.org for axis 0
+                        const int ri = e.nrd++;
+                        e.rd[ri] = d;
+                        const int tx = (d.hi[0] - d.x_base + P1C::TX - 1) / P1C::TX;
+                        const int ty = (d.hi[1] - d.lo[1] + P1C::TY - 1) / P1C::TY;
+                        // z runs: one item spans the whole run (the dpsi_z window)
+                        if (ax == 2 && (d.lo[2] != r.lo || d.hi[2] != r.hi))
+                            raise(ST_INVAL, "pass 1 z range must not cut a z damping run");
+                        for (int b = 0; b < ty; ++b)
+                            for (int a = 0; a < tx; ++a) {
+                                if (ax == 2)
+                                    zitems.push_back(make_int4(ri | (a << 3), b, d.lo[2], d.hi[2]));
+                                else
+                                    tiles.push_back(Item{ri | (a << 3), b, d.lo[2], d.hi[2]});
+                            }
                     }
-                auto& e = pass1_cache_[key];
-                e.runs.set(runs, stream_setup_);
+                std::vector<int4> items;
+                wave_items(tiles, sms_ * p1_per_sm_, p1_zt_, items);
+                items.insert(items.begin(), zitems.begin(), zitems.end());  // longest first
+                e.nitems = (int)items.size();
+                e.ctas = std::max(1, std::min(sms_ * p1_per_sm_, e.nitems));
                 e.items.set(items, stream_setup_);
-                e.count = (int)items.size();
+                e.ctr.set(std::vector<int>{0, 0}, stream_setup_);
                 it = pass1_cache_.find(key);
             }
             auto& e = it->second;
-            if (e.count == 0) return;
+            if (e.nitems == 0) return;
+            refresh_run_maps(p);
+            const int bc = buf_index(p.pc);
+            p1maps_.px = p1x_[bc];
+            p1maps_.py = p1y_[bc];
+            p1maps_.pz = p1z_[bc];
+            P1Params pp;
+            std::memset(&pp, 0, sizeof pp);
+            pp.lay = lay_;
+            for (int i = 0; i < e.nrd; ++i) pp.rd[i] = e.rd[i];
+            for (int a = 0; a < 3; ++a) {
+                pp.run[a][0] = p.run[a][0];
+                pp.run[a][1] = p.run[a][1];
+                pp.ta[a] = p.ta[a];
+                pp.tb[a] = p.tb[a];
+                for (int m = 0; m < kMaxR; ++m) pp.c1[a][m] = p.c1[a][m];
+            }
+            pp.items = e.items.ptr;
+            pp.wq = WorkQueue{e.ctr.ptr, e.nitems};
+            pp.dpz[0] = dpz_[0].ptr;
+            pp.dpz[1] = dpz_[1].ptr;
             if (order_ == 2)
-                k_pass1<R, 2><<<e.count, 256, 0, s>>>(p, e.runs.ptr, e.items.ptr, e.count);
+                k_p1<R, 2><<<e.ctas, P1C::NT, P1C::SMEM, s>>>(p1maps_, pp);
             else
-                k_pass1<R, 1><<<e.count, 256, 0, s>>>(p, e.runs.ptr, e.items.ptr, e.count);
+                k_p1<R, 1><<<e.ctas, P1C::NT, P1C::SMEM, s>>>(p1maps_, pp);
             note_launches(1);
             MM_CUDA(cudaGetLastError());
         }
     }
 
     struct Pass1Work {
-        DArr<RunDesc> runs;
+        RunDesc rd[6];
+        int nrd = 0;
         DArr<int4> items;
-        int count = 0;
+        DArr<int> ctr;
+        int nitems = 0;
+        int ctas = 0;
     };
 
     Layout lay_;
@@ -539,9 +647,17 @@ private:
     int sms_ = 148, inner_per_sm_ = 1, bnd_per_sm_ = 1;
     int order_ = 2;
     bool concurrent_ = false;  // MM_CONCURRENT=1: interior on a side stream, SMs split
+    double inner_zt_ = 48.0, bnd_zt_ = 48.0;
     const float* bufs_[3];
     CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;
     BndMaps maps_;
+    P1Maps p1maps_;
+    DArr<float> dpz_[2];
+    int dz_lo_[2] = {0, 0}, dz_hi_[2] = {0, 0};
+    bool dpz_valid_ = false, zmix_ = false;
+    CUtensorMap p1x_[3], p1y_[3], p1z_[3];
+    int p1_per_sm_ = 1;
+    double p1_zt_ = 16.0;
     CpmlRun runs_[3][2] = {};
     bool runs_valid_ = false;
     cudaStream_t side_ = nullptr, stream_setup_ = nullptr;
