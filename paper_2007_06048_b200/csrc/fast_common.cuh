@@ -114,6 +114,34 @@ __device__ __forceinline__ float comp(const float4& v, int e) {
     return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
 }
 
+// CPML run membership and 4-point (float4) global access helpers
+__device__ __forceinline__ bool in_run(const CpmlRun& r, int l) { return l >= r.lo && l < r.hi; }
+__device__ __forceinline__ bool near_run(const CpmlRun& r, int a, int b) {
+    return r.hi > r.lo && a < r.hi && b > r.lo;  // [a, b) meets the run
+}
+__device__ __forceinline__ float4 ldg4(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+}
+// 16-byte load of 4 points, element-wise (zeros elsewhere) at a box edge
+__device__ __forceinline__ float4 ld4(const float* p, const bool (&ok)[4], bool all) {
+    if (all) return ldg4(p);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok[0]) v.x = __ldg(p);
+    if (ok[1]) v.y = __ldg(p + 1);
+    if (ok[2]) v.z = __ldg(p + 2);
+    if (ok[3]) v.w = __ldg(p + 3);
+    return v;
+}
+__device__ __forceinline__ void st4(float* p, const float (&v)[4], const bool (&ok)[4], bool all) {
+    if (all) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (ok[e]) p[e] = v[e];
+    }
+}
+
 // Arithmetic of the fast kernels, by association order ORD:
 //  ORD 2 (default): the reference's order with every operation separately
 //         rounded (no FMA contraction) -- bit-identical to the CPU reference

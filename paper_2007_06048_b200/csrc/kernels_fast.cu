@@ -1,11 +1,12 @@
 // kernels_fast.cu -- MM_MODE_FAST step: plan (tensor maps, work lists) + launches.
 //
-// One step = pass 1 (psi) -> boundary (CPML pass 2) on the main stream, the
-// interior kernel concurrently on a side stream (it needs no CPML state),
-// then the source injection after the join.  The interior and boundary
-// kernels are persistent: their grids split the GPU's CTA slots in
-// proportion to their algorithmic bytes so both finish together.
-// Kernels: fast_inner.cuh (k_inner), fast_boundary.cuh (k_bnd), fast_pass1.cuh (k_p1).
+// One step = k_p1 (CPML pass 1: psi, and dpsi_z of the z runs) -> k_bnd (pass 2
+// over the X and Y slabs) -> k_inner (the inner x-y box over every z: plain
+// update inside, pass 2 along z in the Z slabs) -> source injection, each
+// kernel persistent over the whole GPU, pulling (tile, z-chunk) work items.
+// Kernels: fast_pass1.cuh (k_p1), fast_boundary.cuh (k_bnd), fast_inner.cuh (k_inner).
+// When the fast CPML kernels cannot serve a layout (radius 8, or z runs closer
+// than 2R), pass 1 and the slabs run the strict kernels and k_inner the inner box.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -181,21 +182,23 @@ public:
             return v ? std::max(1.0, std::atof(v)) : d;
         };
         inner_zt_ = envf("MM_INNER_ZT", 48.0);
-        bnd_zt_ = envf("MM_BND_ZT", 24.0);
+        bnd_zt_ = envf("MM_BND_ZT", 12.0);
         p1_zt_ = envf("MM_P1_ZT", 16.0);
-        const char* conc = std::getenv("MM_CONCURRENT");
-        concurrent_ = conc && conc[0] == '1';
+        // Z slabs: 0 = k_bnd tiles, 1 = k_zslab over the Z slabs after k_inner,
+        // 2 = k_zslab over whole z columns of the inner box (instead of k_inner)
+        if (const char* zm = std::getenv("MM_ZSLABS")) zmode_ = std::max(0, std::min(2, std::atoi(zm)));
         cudaDeviceProp prop;
         MM_CUDA(cudaGetDeviceProperties(&prop, device));
         sms_ = prop.multiProcessorCount;
-        MM_CUDA(cudaFuncSetAttribute(k_inner<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)IC::SMEM));
-        MM_CUDA(cudaFuncSetAttribute(k_inner<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)IC::SMEM));
-        MM_CUDA(cudaFuncSetAttribute(k_inner<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)IC::SMEM));
+        for (auto fn : {k_inner<R, 0>, k_inner<R, 1>, k_inner<R, 2>})
+            MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)IC::SMEM));
+        if constexpr (kBnd)
+            for (auto fn : {k_zslab<R, 0>, k_zslab<R, 1>, k_zslab<R, 2>})
+                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)ZSlabCfg<R>::SMEM));
         int per_sm = 0;
-        MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inner<R, 1>, IC::NT,
+        MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inner<R, 2>, IC::NT,
                                                               IC::SMEM));
         inner_per_sm_ = std::max(1, per_sm);
         if constexpr (kBnd) {
@@ -216,49 +219,35 @@ public:
                                                                   P1C::SMEM));
             p1_per_sm_ = std::max(1, per_sm);
         }
-        MM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
-        MM_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
-        MM_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
     }
-    ~FastPlanR() override {
-        cudaEventDestroy(fork_);
-        cudaEventDestroy(join_);
-        cudaStreamDestroy(side_);
-    }
+    ~FastPlanR() override = default;
 
     void pass1(const StepParams& p, cudaStream_t s) override { launch_pass1(p, 0, lay_.n[2], s); }
 
     void update(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t s) override {
-        if (region == 0) {
-            MM_CUDA(cudaEventRecord(fork_, s));
-            MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
-            launch_inner(p, z_lo, z_hi, true, side_);
-            launch_boundary(p, z_lo, z_hi, true, s);
-            MM_CUDA(cudaEventRecord(join_, side_));
-            MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
-        } else if (region == 1) {
-            launch_inner(p, z_lo, z_hi, false, s);
-        } else {
-            launch_boundary(p, z_lo, z_hi, false, s);
+        const bool fc = fast_cpml(p);
+        if (region == 0 || region == 1)
+            launch_inner(p, z_lo, z_hi, region == 0 && fc && zmode_ != 0 ? kFull : kInnerOnly, s);
+        if (region == 0 || region == 2) {
+            if (fc) {
+                launch_boundary(p, z_lo, z_hi, s);  // X and Y slabs
+                if (region == 2 && zmode_ != 0) launch_inner(p, z_lo, z_hi, kZSlabs, s);
+            } else {
+                strict_update(p, 2, z_lo, z_hi, s);
+            }
         }
     }
 
     void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
               const int* step_dev, cudaStream_t s) override {
-        if (!concurrent_) {  // default: each kernel gets the whole GPU, in turn
-            launch_pass1(p, 0, lay_.n[2], s);
-            launch_boundary(p, 0, lay_.n[2], false, s);
-            launch_inner(p, 0, lay_.n[2], false, s);
-            if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
-            return;
-        }
-        MM_CUDA(cudaEventRecord(fork_, s));
-        MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
-        launch_inner(p, 0, lay_.n[2], true, side_);
+        // each kernel gets the whole GPU, in turn
+        const bool fc = fast_cpml(p);
         launch_pass1(p, 0, lay_.n[2], s);
-        launch_boundary(p, 0, lay_.n[2], true, s);
-        MM_CUDA(cudaEventRecord(join_, side_));
-        MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
+        if (fc)
+            launch_boundary(p, 0, lay_.n[2], s);
+        else
+            strict_update(p, 2, 0, lay_.n[2], s);
+        launch_inner(p, 0, lay_.n[2], fc && zmode_ != 0 ? kFull : kInnerOnly, s);
         if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
     }
 
@@ -307,43 +296,12 @@ private:
         int nbox = 0;
     };
 
-    // CTA budgets.  Alone, a kernel gets every SM; when the interior and
-    // boundary kernels run concurrently the SMs are split in proportion to
-    // their algorithmic bytes so both finish together.
-    void budgets(const StepParams& p, int z_lo, int z_hi, bool conc, int& gi, int& gb) const {
-        if (!conc) {
-            gi = sms_ * inner_per_sm_;
-            gb = sms_ * bnd_per_sm_;
-            return;
-        }
-        Box inner;
-        std::vector<std::pair<int, Box>> slabs;
-        regions(p, inner, slabs);
-        auto vol = [&](const Box& b) {
-            const long long zl = std::max(b.lo[2], z_lo), zh = std::min(b.hi[2], z_hi);
-            if (zh <= zl) return 0.0;
-            return (double)(b.hi[0] - b.lo[0]) * (b.hi[1] - b.lo[1]) * (zh - zl);
-        };
-        const double wi = 16.0 * vol(inner);
-        double wb = 0;
-        for (const auto& s : slabs) wb += 34.0 * vol(s.second);
-        if (!kBnd) wb *= 4.0;  // strict boundary kernel is slower
-        if (wb <= 0) {
-            gi = sms_ * inner_per_sm_;
-            gb = 0;
-        } else if (wi <= 0) {
-            gi = 0;
-            gb = sms_ * bnd_per_sm_;
-        } else {
-            const int si = std::min(sms_ - 1,
-                                    std::max(1, (int)std::lround(sms_ * wi / (wi + wb))));
-            gi = si * inner_per_sm_;
-            gb = (sms_ - si) * bnd_per_sm_;
-        }
-    }
+    // inner-kernel domains: the inner box, inner box + Z slabs (one z column),
+    // Z slabs only
+    enum InnerMode { kInnerOnly = 0, kFull = 1, kZSlabs = 2 };
 
-    static long long wkey(int z_lo, int z_hi, bool conc) {
-        return ((long long)z_lo << 32) ^ ((long long)z_hi << 1) ^ (conc ? 1 : 0);
+    static long long wkey(int z_lo, int z_hi, int mode) {
+        return ((long long)z_lo << 32) ^ ((long long)z_hi << 2) ^ mode;
     }
 
     void finish_work(Work& w, const std::vector<Item>& tiles, int ctas, double target) {
@@ -355,35 +313,45 @@ private:
         w.ctr.set(std::vector<int>{0, 0}, stream_setup_);
     }
 
-    Work& inner_work(const StepParams& p, int z_lo, int z_hi, bool conc) {
-        const auto key = wkey(z_lo, z_hi, conc);
+    Work& inner_work(const StepParams& p, int z_lo, int z_hi, int mode) {
+        const auto key = wkey(z_lo, z_hi, mode);
         auto it = inner_cache_.find(key);
         if (it != inner_cache_.end()) return it->second;
         Work& w = inner_cache_[key];
         Box inner;
         std::vector<std::pair<int, Box>> slabs;
         regions(p, inner, slabs);
-        inner.lo[2] = std::max(inner.lo[2], z_lo);
-        inner.hi[2] = std::min(inner.hi[2], z_hi);
-        w.box = inner;
-        if (inner.hi[0] <= inner.lo[0] || inner.hi[1] <= inner.lo[1] || inner.hi[2] <= inner.lo[2])
-            return w;
+        w.box = inner;  // x-y box of the tiles; z = the inner z range
+        if (inner.hi[0] <= inner.lo[0] || inner.hi[1] <= inner.lo[1]) return w;
+        // z ranges of this launch
+        std::vector<std::pair<int, int>> zr;
+        auto add = [&](int a, int b) {
+            a = std::max(a, z_lo);
+            b = std::min(b, z_hi);
+            if (b > a) zr.emplace_back(a, b);
+        };
+        if (mode == kInnerOnly) add(inner.lo[2], inner.hi[2]);
+        if (mode == kFull) add(0, lay_.n[2]);
+        if (mode == kZSlabs) {
+            add(0, inner.lo[2]);
+            add(inner.hi[2], lay_.n[2]);
+        }
+        if (zr.empty()) return w;
         w.empty = false;
         w.x_base = inner.lo[0] & ~3;
         const int tiles_x = (inner.hi[0] - w.x_base + IC::TX - 1) / IC::TX;
         const int tiles_y = (inner.hi[1] - inner.lo[1] + IC::TY - 1) / IC::TY;
         std::vector<Item> tiles;
-        for (int ty = 0; ty < tiles_y; ++ty)
-            for (int tx = 0; tx < tiles_x; ++tx)
-                tiles.push_back(Item{tx, ty, inner.lo[2], inner.hi[2]});
-        int gi, gb;
-        budgets(p, z_lo, z_hi, conc, gi, gb);
-        finish_work(w, tiles, std::max(1, gi), inner_zt_);
+        for (const auto& r : zr)
+            for (int ty = 0; ty < tiles_y; ++ty)
+                for (int tx = 0; tx < tiles_x; ++tx) tiles.push_back(Item{tx, ty, r.first, r.second});
+        finish_work(w, tiles, sms_ * inner_per_sm_, inner_zt_);
         return w;
     }
 
-    Work& bnd_work(const StepParams& p, int z_lo, int z_hi, bool conc) {
-        const auto key = wkey(z_lo, z_hi, conc);
+    // X and Y slabs (the Z slabs go with the inner kernel)
+    Work& bnd_work(const StepParams& p, int z_lo, int z_hi) {
+        const auto key = wkey(z_lo, z_hi, 0);
         auto it = bnd_cache_.find(key);
         if (it != bnd_cache_.end()) return it->second;
         Work& w = bnd_cache_[key];
@@ -398,7 +366,7 @@ private:
             return e ? std::atoi(e) : 7;
         }();
         for (const auto& s : slabs) {
-            if (!((kinds >> (s.first / 2)) & 1)) continue;
+            if ((s.first / 2 == 2 && zmode_ != 0) || !((kinds >> (s.first / 2)) & 1)) continue;
             const Box& b = s.second;
             const int zl = std::max(b.lo[2], z_lo), zh = std::min(b.hi[2], z_hi);
             if (zh <= zl) continue;
@@ -419,14 +387,17 @@ private:
         }
         if (items.empty()) return w;
         w.empty = false;
-        int gi, gb;
-        budgets(p, z_lo, z_hi, conc, gi, gb);
-        finish_work(w, items, std::max(1, gb), bnd_zt_);
+        finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_);
         return w;
     }
 
-    void launch_inner(const StepParams& p, int z_lo, int z_hi, bool conc, cudaStream_t s) {
-        Work& w = inner_work(p, z_lo, z_hi, conc);
+    void launch_inner(const StepParams& p, int z_lo, int z_hi, int mode, cudaStream_t s) {
+        if (mode == kFull && zmode_ == 1) {  // inner box and Z slabs separately
+            launch_inner(p, z_lo, z_hi, kInnerOnly, s);
+            launch_inner(p, z_lo, z_hi, kZSlabs, s);
+            return;
+        }
+        Work& w = inner_work(p, z_lo, z_hi, mode);
         if (w.empty) return;
         InnerParams ip;
         std::memset(&ip, 0, sizeof ip);
@@ -447,13 +418,36 @@ private:
             sum += p.c2[0][m] + p.c2[1][m] + p.c2[2][m];
         }
         ip.center = -2.0f * sum;
+        ip.zi_lo = w.box.lo[2];
+        ip.zi_hi = w.box.hi[2];
+        ip.tik_x = p.tik[0];
+        ip.tik_y = p.tik[1];
+        ip.ta_z = p.ta[2];
+        ip.tb_z = p.tb[2];
+        ip.tik_z = p.tik[2];
+        for (int sd = 0; sd < 2; ++sd) {
+            ip.zrun[sd] = p.run[2][sd];
+            ip.dpz[sd] = dpz_[sd].ptr;
+            ip.dz_lo[sd] = dz_lo_[sd];
+            ip.dz_hi[sd] = dz_hi_[sd];
+        }
         const int bc = buf_index(p.pc), bp = buf_index(p.pp);
-        if (order_ == 2)
-            k_inner<R, 2><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
-        else if (order_ == 1)
-            k_inner<R, 1><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
-        else
-            k_inner<R, 0><<<w.ctas, IC::NT, IC::SMEM, s>>>(in_halo_[bc], in_tile_[bp], cv_in_, ip);
+        const CUtensorMap &a = in_halo_[bc], &b = in_tile_[bp];
+        if (mode != kInnerOnly) {  // column kernel (only with the fast CPML kernels: R <= 4)
+            constexpr size_t zsm = ZSlabCfg<R>::SMEM;
+            if (order_ == 2)
+                k_zslab<R, 2><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+            else if (order_ == 1)
+                k_zslab<R, 1><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+            else
+                k_zslab<R, 0><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+        } else if (order_ == 2) {
+            k_inner<R, 2><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
+        } else if (order_ == 1) {
+            k_inner<R, 1><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
+        } else {
+            k_inner<R, 0><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
+        }
         note_launches(1);
         MM_CUDA(cudaGetLastError());
     }
@@ -494,31 +488,29 @@ private:
             for (int sd = 0; sd < 2; ++sd) {
                 const CpmlRun& r = p.run[a][sd];
                 runs_[a][sd] = r;
-                int bx = BC::TX, by = BC::TY;
-                if (a == 0) bx = BC::BX;  // x halo
-                if (a == 1) by = BC::BY;  // y halo
-                maps_.psi[a][sd] = run_map(lay_, r, a, r.psi, bx, by);
+                if (a == 0) maps_.psi[0][sd] = run_map(lay_, r, a, r.psi, BC::BX, BC::TY);  // x halo
+                if (a == 1) maps_.psi[1][sd] = run_map(lay_, r, a, r.psi, BC::TX, BC::BY);  // y halo
                 maps_.zeta[a][sd] = run_map(lay_, r, a, r.zeta, BC::TX, BC::TY);
                 p1maps_.psi[a][sd] = run_map(lay_, r, a, r.psi, P1C::TX, P1C::TY);
             }
         runs_valid_ = true;
     }
 
-    void launch_boundary(const StepParams& p, int z_lo, int z_hi, bool conc, cudaStream_t s) {
-        if constexpr (!(kBnd && kP1)) {
-            strict_update(p, 2, z_lo, z_hi, s);
-            return;
-        } else {
-            if (!ensure_dpz(p)) {
-                strict_update(p, 2, z_lo, z_hi, s);
-                return;
-            }
-            Work& w = bnd_work(p, z_lo, z_hi, conc);
+    // fast CPML: k_p1 + k_bnd + the inner kernel's Z-slab planes
+    bool fast_cpml(const StepParams& p) {
+        if constexpr (!(kBnd && kP1))
+            return false;
+        else
+            return ensure_dpz(p);
+    }
+
+    void launch_boundary(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) {
+        if constexpr (kBnd && kP1) {
+            Work& w = bnd_work(p, z_lo, z_hi);
             if (w.empty) return;
             refresh_run_maps(p);
-            const int bc = buf_index(p.pc), bp = buf_index(p.pp);
-            maps_.pc = bd_halo_[bc];
-            maps_.pp = bd_tile_[bp];
+            maps_.pc = bd_halo_[buf_index(p.pc)];
+            maps_.pp = bd_tile_[buf_index(p.pp)];
             maps_.cv = cv_bd_;
             BndParams bp_;
             std::memset(&bp_, 0, sizeof bp_);
@@ -537,9 +529,12 @@ private:
                 }
             }
             for (int sd = 0; sd < 2; ++sd) {
+                bp_.dpz[sd] = dpz_[sd].ptr;
                 bp_.dz_lo[sd] = dz_lo_[sd];
                 bp_.dz_hi[sd] = dz_hi_[sd];
             }
+            bp_.pp = p.pp;
+            bp_.cv = p.cv;
             bp_.pn = p.pn;
             bp_.segs = w.segs.ptr;
             bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
@@ -557,7 +552,7 @@ private:
             strict_pass1(p, z_lo, z_hi, s);
             return;
         } else {
-            if (!ensure_dpz(p)) {
+            if (!fast_cpml(p)) {
                 strict_pass1(p, z_lo, z_hi, s);
                 return;
             }
@@ -567,10 +562,15 @@ private:
                 Pass1Work& e = pass1_cache_[key];
                 std::vector<Item> tiles;
                 std::vector<int4> zitems;
+                // MM_P1_AXES (profiling only): bit mask of the run axes to update
+                static const int axes = [] {
+                    const char* e = std::getenv("MM_P1_AXES");
+                    return e ? std::atoi(e) : 7;
+                }();
                 for (int ax = 0; ax < 3; ++ax)
                     for (int side = 0; side < 2; ++side) {
                         const CpmlRun& r = p.run[ax][side];
-                        if (r.hi <= r.lo) continue;
+                        if (r.hi <= r.lo || !((axes >> ax) & 1)) continue;
                         RunDesc d{ax, side, {0, 0, 0}, {lay_.n[0], lay_.n[1], lay_.n[2]}, 0};
                         d.lo[ax] = r.lo;
                         d.hi[ax] = r.hi;
@@ -646,8 +646,8 @@ private:
     int device_;
     int sms_ = 148, inner_per_sm_ = 1, bnd_per_sm_ = 1;
     int order_ = 2;
-    bool concurrent_ = false;  // MM_CONCURRENT=1: interior on a side stream, SMs split
     double inner_zt_ = 48.0, bnd_zt_ = 48.0;
+    int zmode_ = 0;
     const float* bufs_[3];
     CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;
     BndMaps maps_;
@@ -660,8 +660,7 @@ private:
     double p1_zt_ = 16.0;
     CpmlRun runs_[3][2] = {};
     bool runs_valid_ = false;
-    cudaStream_t side_ = nullptr, stream_setup_ = nullptr;
-    cudaEvent_t fork_ = nullptr, join_ = nullptr;
+    cudaStream_t stream_setup_ = nullptr;
     std::map<long long, Work> inner_cache_, bnd_cache_;
     std::map<std::pair<int, int>, Pass1Work> pass1_cache_;
 };
