@@ -78,19 +78,21 @@ def byte_model(n, nd, r=4):
     return 16.0 * N + 16.0 * damped, N, damped
 
 
-def kernel_bytes(n, nd):
+def kernel_bytes(n, nd, r=4):
     """Algorithmic bytes per launch of the three step kernels:
       inner    16 B per inner-box point (p_cur, p_prev, c read; p_next write)
-      boundary 16 B per slab point + 12 B per damped-axis point (psi read,
-               zeta read + write)
+      boundary 16 B per slab point + 12 B per damped-axis point (psi or dpsi_z
+               read, zeta read + write)
       pass1    8 B per damped-axis point (psi read + write) + 4 B per slab
-               point (p_cur read)"""
+               point (p_cur read) + 4 B per dpsi_z point written (the z runs
+               widened by R planes on both sides)"""
     N = float(n[0]) * n[1] * n[2]
     damped = sum(N * 2 * nd[a] / n[a] for a in range(3))
     inner = float(np.prod([n[a] - 2 * nd[a] for a in range(3)]))
     slab = N - inner
+    dpz = 2.0 * (nd[2] + 2 * r) * n[0] * n[1] if nd[2] > 0 else 0.0
     return {"inner": 16.0 * inner, "boundary": 16.0 * slab + 12.0 * damped,
-            "pass1": 8.0 * damped + 4.0 * slab}
+            "pass1": 8.0 * damped + 4.0 * slab + 4.0 * dpz}
 
 
 # ------------------------------------------------------------------ clocks
