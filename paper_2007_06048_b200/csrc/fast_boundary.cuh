@@ -52,7 +52,11 @@ struct BndCfg {
     static constexpr int NS = MM_BND_NS > 2 * R + 1 ? MM_BND_NS : 2 * R + 2;
     static constexpr int NQD = 8;  // stage barriers: at most NQD stages in flight
     static constexpr int NBAR = 2 * NS + 2 * NQD + 4;
-    static constexpr int BUDGET = 112 * 1024;  // bytes per CTA: two CTAs per SM
+    // bytes per CTA: two CTAs per SM up to R = 4; one (with the registers of
+    // two) for wider stencils, whose z window needs a deeper ring
+    static constexpr int CTAS = R <= 4 ? 2 : 1;
+    static constexpr int BUDGET = CTAS == 2 ? 112 * 1024 : 220 * 1024;
+    static constexpr int MAXREG = CTAS == 2 ? 128 : 255;
     static constexpr int QB_RAW = (BUDGET - 4 * NS * PPLANE - 8 * NBAR - 4 * NQD - 64) / 4;
     static constexpr int QMAX = 7 * TILE + PSX + 2 * PSY;
     static constexpr int QB = QB_RAW > QMAX ? QB_RAW / 32 * 32 : QMAX;
@@ -158,12 +162,9 @@ __device__ __forceinline__ uint32_t q_alloc(uint32_t& V, int size, int qb) {
     return v;
 }
 
-#ifndef MM_BND_MAXREG
-#define MM_BND_MAXREG 128
-#endif
 template <int R, int ORD>
 // Register cap for two CTAs of 8 warps per SM (see k_inner).
-__global__ void __maxnreg__(MM_BND_MAXREG)
+__global__ void __maxnreg__(BndCfg<R>::MAXREG)
     k_bnd(const __grid_constant__ BndMaps M, const BndParams P) {
     using C = BndCfg<R>;
     extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -155,7 +155,8 @@ class FastPlanR final : public FastPlan {
     using IC = InnerCfg<R>;
     using BC = BndCfg<R>;
     using P1C = P1Cfg<R>;
-    static constexpr bool kBnd = R <= 4;  // TMA boundary kernel (R = 8: strict kernels)
+    static constexpr bool kBnd = BC::SMEM <= 227 * 1024;  // TMA boundary kernel fits
+    static constexpr bool kZs = ZSlabCfg<R>::SMEM <= 227 * 1024;  // optional Z-slab kernel
     static constexpr bool kP1 = P1C::SMEM <= 200 * 1024;
 
 public:
@@ -187,13 +188,14 @@ public:
         // Z slabs: 0 = k_bnd tiles, 1 = k_zslab over the Z slabs after k_inner,
         // 2 = k_zslab over whole z columns of the inner box (instead of k_inner)
         if (const char* zm = std::getenv("MM_ZSLABS")) zmode_ = std::max(0, std::min(2, std::atoi(zm)));
+        if (!kZs) zmode_ = 0;
         cudaDeviceProp prop;
         MM_CUDA(cudaGetDeviceProperties(&prop, device));
         sms_ = prop.multiProcessorCount;
         for (auto fn : {k_inner<R, 0>, k_inner<R, 1>, k_inner<R, 2>})
             MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)IC::SMEM));
-        if constexpr (kBnd)
+        if constexpr (kZs)
             for (auto fn : {k_zslab<R, 0>, k_zslab<R, 1>, k_zslab<R, 2>})
                 MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)ZSlabCfg<R>::SMEM));
@@ -433,14 +435,16 @@ private:
         }
         const int bc = buf_index(p.pc), bp = buf_index(p.pp);
         const CUtensorMap &a = in_halo_[bc], &b = in_tile_[bp];
-        if (mode != kInnerOnly) {  // column kernel (only with the fast CPML kernels: R <= 4)
-            constexpr size_t zsm = ZSlabCfg<R>::SMEM;
-            if (order_ == 2)
-                k_zslab<R, 2><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
-            else if (order_ == 1)
-                k_zslab<R, 1><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
-            else
-                k_zslab<R, 0><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+        if (mode != kInnerOnly) {  // column kernel (MM_ZSLABS = 1, 2)
+            if constexpr (kZs) {
+                constexpr size_t zsm = ZSlabCfg<R>::SMEM;
+                if (order_ == 2)
+                    k_zslab<R, 2><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+                else if (order_ == 1)
+                    k_zslab<R, 1><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+                else
+                    k_zslab<R, 0><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+            }
         } else if (order_ == 2) {
             k_inner<R, 2><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
         } else if (order_ == 1) {
