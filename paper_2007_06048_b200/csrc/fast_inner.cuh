@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, InnerCfg<R>::MINB)
 template <int R>
 struct ZSlabCfg {
     using I = InnerCfg<R>;
-    static constexpr int NS = 2 * R + 1 + 3;
-    static constexpr int NQ = 4;
+    static constexpr int NS = 2 * R + 1 + (R <= 4 ? 3 : 2);
+    static constexpr int NQ = R <= 4 ? 4 : 2;
     static constexpr size_t SMEM =
         sizeof(float) * (size_t)(NS * I::PLANE + NQ * 2 * I::TILE) + 8 * (NS + NQ) + 16;
 };

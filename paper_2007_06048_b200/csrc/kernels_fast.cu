@@ -189,6 +189,11 @@ public:
         // 2 = k_zslab over whole z columns of the inner box (instead of k_inner)
         if (const char* zm = std::getenv("MM_ZSLABS")) zmode_ = std::max(0, std::min(2, std::atoi(zm)));
         if (!kZs) zmode_ = 0;
+        // R > 4: the interior kernel's z loop unrolled by 2R+1 overflows the
+        // instruction cache; the column kernel (smem z window) serves the inner
+        // box and the Z slabs instead
+        col_inner_ = kZs && R > 4;
+        if (col_inner_ && !std::getenv("MM_ZSLABS")) zmode_ = 2;
         cudaDeviceProp prop;
         MM_CUDA(cudaGetDeviceProperties(&prop, device));
         sms_ = prop.multiProcessorCount;
@@ -435,7 +440,7 @@ private:
         }
         const int bc = buf_index(p.pc), bp = buf_index(p.pp);
         const CUtensorMap &a = in_halo_[bc], &b = in_tile_[bp];
-        if (mode != kInnerOnly) {  // column kernel (MM_ZSLABS = 1, 2)
+        if (mode != kInnerOnly || col_inner_) {  // column kernel (MM_ZSLABS = 1, 2; R > 4)
             if constexpr (kZs) {
                 constexpr size_t zsm = ZSlabCfg<R>::SMEM;
                 if (order_ == 2)
@@ -652,6 +657,7 @@ private:
     int order_ = 2;
     double inner_zt_ = 48.0, bnd_zt_ = 48.0;
     int zmode_ = 0;
+    bool col_inner_ = false;
     const float* bufs_[3];
     CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;
     BndMaps maps_;
