@@ -299,7 +299,7 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
     const int soff = (R + ty) * C::BX + C::HX + 4 * tx;  // in a p_cur plane
     unsigned ni = 0, nq = 0;
     unsigned s = 0, ph = 0;  // ring slot / parity of the next plane to arrive
-    uint32_t V = 0;          // stage allocator, in step with the producer's
+    int qo = 0;              // stage offset in the circular buffer (the producer's V % QB)
 
     for (;;) {
         int4 sg;
@@ -350,31 +350,38 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
         const int psx_off = ty * C::BX + C::HX + 4 * tx;    // in the psi_x box
         const int toff = ty * C::TX + 4 * tx;               // in a tile
         const int psy_off = (R + ty) * C::TX + 4 * tx;      // in a psi_y box
+        // zeta_z of the two z runs at plane zb (same x/y strides)
+        auto zz_at_zb = [&](int sd) {
+            return P.run[2][sd].hi > P.run[2][sd].lo
+                       ? P.run[2][sd].zeta + run_off(P.run[2][sd], 2, xg, y, T.zb)
+                       : nullptr;
+        };
+        float* const zzb0 = zz_at_zb(0);
+        float* const zzb1 = zz_at_zb(1);
+        const long long zz_step = P.run[2][0].hi > P.run[2][0].lo ? P.run[2][0].s2 : P.run[2][1].s2;
+        // z window: shared-memory offsets of this thread's points in planes
+        // j-2R .. j, rotated by one slot per plane (no modular slot arithmetic)
+        int wo[2 * R + 1];
+        int rel = (int)s;  // slot of the oldest window plane (next to release)
 
 #pragma unroll 1
         for (int j = 0; j < T.nring; ++j) {
+#pragma unroll
+            for (int k = 0; k < 2 * R; ++k) wo[k] = wo[k + 1];
+            wo[2 * R] = (int)s * C::PPLANE + soff;
             if (j >= 2 * R) {
                 const int o = j - 2 * R;
                 const int z = T.zb + o;
                 const long long fo = (long long)o * L.plane;
                 const int zr = zrun_of(P, z);
                 const int zex = zext_of(P, z);
-                float* zz_p = zr >= 0 ? P.run[2][zr].zeta + run_off(P.run[2][zr], 2, xg, y, z)
-                                      : nullptr;
+                float* zz_p = (zr == 0 ? zzb0 : zzb1) + o * zz_step;
                 const float aza = __ldg(P.ta[2] + z), azb = __ldg(P.tb[2] + z),
                             azk = __ldg(P.tik[2] + z);
 
                 mbar_wait(fullP + 8 * s, ph);
                 // centre plane j - R, window planes j - 2R .. j
-                int cs = (int)s - R;
-                if (cs < 0) cs += C::NS;
-                auto slot_of = [&](int m) {  // slot of plane j - R + m
-                    int t = cs + m;
-                    if (t >= C::NS) t -= C::NS;
-                    if (t < 0) t += C::NS;
-                    return t;
-                };
-                const float* S = ring + cs * C::PPLANE + soff;
+                const float* S = ring + wo[R];
                 float xs[4 + 2 * C::HX];
 #pragma unroll
                 for (int h = 0; h < (4 + 2 * C::HX) / 4; ++h) {
@@ -406,8 +413,8 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                 }
 #pragma unroll
                 for (int m = 1; m <= R; ++m) {
-                    const float4 u = lds4(ring + slot_of(m) * C::PPLANE + soff);
-                    const float4 d = lds4(ring + slot_of(-m) * C::PPLANE + soff);
+                    const float4 u = lds4(ring + wo[R + m]);
+                    const float4 d = lds4(ring + wo[R - m]);
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
                         d2z[e] = d2_term<ORD>(d2z[e], P.c2[2][m - 1], comp(u, e), comp(d, e),
@@ -418,9 +425,10 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                 float4 pp, cv, zx = make_float4(0.f, 0.f, 0.f, 0.f), zy = zx, zz = zx, dz = zx;
                 {
                     const int st = nq % C::NQD;
-                    const float* Q =
-                        qring + q_alloc(V, T.qsize + (zr >= 0 ? C::TILE : 0) + (zex >= 0 ? C::TILE : 0),
-                                        C::QB) % C::QB;
+                    const int qsz = T.qsize + (zr >= 0 ? C::TILE : 0) + (zex >= 0 ? C::TILE : 0);
+                    if (qo + qsz > C::QB) qo = 0;  // a stage never wraps (q_alloc)
+                    const float* Q = qring + qo;
+                    qo += qsz;
                     mbar_wait(fullQ + 8 * st, (nq / C::NQD) & 1);
                     pp = lds4(Q + toff);
                     cv = lds4(Q + C::TILE + toff);
@@ -474,7 +482,8 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                 }
                 // plane j - 2R has had its last use
                 __syncwarp();
-                if (lane == 0) mbar_arrive_b(emptyP + 8 * slot_of(-R));
+                if (lane == 0) mbar_arrive_b(emptyP + 8 * rel);
+                if (++rel == C::NS) rel = 0;
 
                 // reference: drive = d2p*ik + dpsi; zeta = b*zeta + a*drive;
                 // term = drive + zeta; lap = (term_x + term_y) + term_z
@@ -505,11 +514,10 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
         }
         // the item's last 2R planes
 #pragma unroll 1
-        for (int k = 2 * R; k >= 1; --k) {
-            int t = (int)s - k;
-            if (t < 0) t += C::NS;
+        for (int k = 0; k < 2 * R; ++k) {
             __syncwarp();
-            if (lane == 0) mbar_arrive_b(emptyP + 8 * t);
+            if (lane == 0) mbar_arrive_b(emptyP + 8 * rel);
+            if (++rel == C::NS) rel = 0;
         }
     }
 }

@@ -189,6 +189,12 @@ public:
         // 2 = k_zslab over whole z columns of the inner box (instead of k_inner)
         if (const char* zm = std::getenv("MM_ZSLABS")) zmode_ = std::max(0, std::min(2, std::atoi(zm)));
         if (!kZs) zmode_ = 0;
+        { const char* ov = std::getenv("MM_OVERLAP"); overlap_ = !ov || ov[0] != '0'; }
+        if (overlap_) {
+            MM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+            MM_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+            MM_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
+        }
         // R > 4: the interior kernel's z loop unrolled by 2R+1 overflows the
         // instruction cache; the column kernel (smem z window) serves the inner
         // box and the Z slabs instead
@@ -227,7 +233,11 @@ public:
             p1_per_sm_ = std::max(1, per_sm);
         }
     }
-    ~FastPlanR() override = default;
+    ~FastPlanR() override {
+        if (fork_) cudaEventDestroy(fork_);
+        if (join_) cudaEventDestroy(join_);
+        if (side_) cudaStreamDestroy(side_);
+    }
 
     void pass1(const StepParams& p, cudaStream_t s) override { launch_pass1(p, 0, lay_.n[2], s); }
 
@@ -247,14 +257,28 @@ public:
 
     void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
               const int* step_dev, cudaStream_t s) override {
-        // each kernel gets the whole GPU, in turn
         const bool fc = fast_cpml(p);
+        const int imode = fc && zmode_ != 0 ? kFull : kInnerOnly;
+        // (the Z-slab planes read dpsi_z from pass 1: no overlap then)
+        const bool ov = overlap_ && imode == kInnerOnly;
+        if (ov) {
+            // the interior kernel needs no CPML state: it runs on a second
+            // stream beside pass 1 -> boundary and takes SMs as their tails free
+            // them (a second branch of the captured graph)
+            MM_CUDA(cudaEventRecord(fork_, s));
+            MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+            launch_inner(p, 0, lay_.n[2], imode, side_);
+            MM_CUDA(cudaEventRecord(join_, side_));
+        }
         launch_pass1(p, 0, lay_.n[2], s);
         if (fc)
             launch_boundary(p, 0, lay_.n[2], s);
         else
             strict_update(p, 2, 0, lay_.n[2], s);
-        launch_inner(p, 0, lay_.n[2], fc && zmode_ != 0 ? kFull : kInnerOnly, s);
+        if (ov)
+            MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
+        else
+            launch_inner(p, 0, lay_.n[2], imode, s);
         if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
     }
 
@@ -657,6 +681,9 @@ private:
     int order_ = 2;
     double inner_zt_ = 48.0, bnd_zt_ = 48.0;
     int zmode_ = 0;
+    bool overlap_ = false;
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t fork_ = nullptr, join_ = nullptr;
     bool col_inner_ = false;
     const float* bufs_[3];
     CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;
