@@ -3,10 +3,10 @@
 // ref: AcousticCdEngine::update_plain (propagator_impl.hpp:89-104),
 //      laplacian_at (stencil.hpp:70-82).
 //
-// 2.5D streaming along z (the slowest device axis).  One CTA per SM (16
-// warps) pulls (tile, z-chunk) items from a work queue ordered so that the
+// 2.5D streaming along z (the slowest device axis).  Two CTAs per SM (8
+// warps each) pull (tile, z-chunk) items from a work queue ordered so that the
 // items in flight are neighbouring tiles at the same z (halos meet in L2).
-//  * p_cur planes (64 x 32 tile + halo) arrive by TMA (cp.async.bulk.tensor,
+//  * p_cur planes (64 x 16 tile + halo) arrive by TMA (cp.async.bulk.tensor,
 //    mbarrier complete_tx) into a ring of QW = 2R+1 shared slots; ring slot
 //    == register-queue slot == plane index mod QW, so every shared address is
 //    a compile-time offset (the z loop is unrolled by QW).
@@ -28,7 +28,7 @@ struct InnerCfg {
     static constexpr int TXT = 16;               // thread columns, 4 x-points each
     static constexpr int TX = 4 * TXT;           // 64
 #ifndef MM_INNER_TR
-#define MM_INNER_TR 32
+#define MM_INNER_TR 16
 #endif
     static constexpr int TR = R <= 4 ? MM_INNER_TR : 16;  // thread rows (one row each)
     static constexpr int MINB = TR == 32 ? 1 : 2;           // CTAs per SM
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, InnerCfg<R>::MINB)
 // k_zslab streams whole z columns of the inner x-y box: planes inside
 // [zi_lo, zi_hi) get the plain update, the Z-slab planes outside it the pass-2
 // formula along z (update_damping_pass2, propagator_impl.hpp:125-152; dpsi_x,
-// dpsi_y, zeta_x, zeta_y are masked to 0 there).  Same 64 x 32 tiles and TMA
+// dpsi_y, zeta_x, zeta_y are masked to 0 there).  Same 64 x 16 tiles and TMA
 // pipeline as k_inner.  The z window is read from a ring of
 // NS = 2R+1+lead shared slots (no register queue, so the loop is not unrolled
 // and the code stays small), dpsi_z (k_p1) and zeta_z come straight from
