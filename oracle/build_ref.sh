@@ -3,8 +3,9 @@
 # they lie under /root/reference (read-only, never copied), together with
 # oracle/ref_shim.cpp into oracle/_ref/libminimod_ref.so.  Flags match the
 # reference's Release build (-O3 -DNDEBUG -std=gnu++20, no -march: SSE2, no
-# FMA).  nlohmann/json (header-only; needed by source.cpp/model.cpp for I/O we
-# never call) comes from the image's cudnn_frontend wheel (nlohmann 3.11.3).
+# FMA).  nlohmann/json (header-only; source.cpp/model.cpp's shot-record and
+# model-manifest I/O, which the format tests pin against) comes from the
+# image's cudnn_frontend wheel (nlohmann 3.11.3).
 # Test infrastructure only.
 set -euo pipefail
 here="$(cd "$(dirname "$0")" && pwd)"

@@ -174,6 +174,55 @@ class Oracle:
         return dict(traces=traces, dt=dt.value, kernel_seconds=ks.value,
                     modeling_seconds=ms.value)
 
+    # ---- on-disk formats and report (reference back end only) -----------
+    def _ref_only(self):
+        if self.kind != "reference":
+            raise NotImplementedError("the reference back end writes the reference formats")
+
+    def save_record(self, traces, dt, path, *, source_loc=(0, 0, 0), receiver_increment=(1, 1),
+                    nshots=1):
+        """save_record (source.cpp:68-95): traces [nreceivers x nsteps]."""
+        self._ref_only()
+        t = np.ascontiguousarray(traces, dtype=np.float32)
+        self._check(self.lib.ref_save_record(
+            _f32(t), C.c_int(t.shape[0]), C.c_int(t.shape[1]), C.c_double(dt), _i3(*source_loc),
+            (C.c_int * 2)(*receiver_increment), C.c_int(nshots), str(path).encode()))
+
+    def save_model(self, vp, n, d, radius, manifest):
+        """save_model (model.cpp:160-190) of a ghosted vp field."""
+        self._ref_only()
+        v = np.ascontiguousarray(vp, dtype=np.float32)
+        self._check(self.lib.ref_save_model(_i3(*n), _d3(*d), C.c_int(radius), _f32(v),
+                                            str(manifest).encode()))
+
+    def load_model(self, manifest, radius=4):
+        """load_model (model.cpp:64-99): (n, d, ghosted vp of radius 4, vmin, vmax)."""
+        self._ref_only()
+        n, d = _i3(), _d3()
+        vmin, vmax = C.c_float(), C.c_float()
+        self._check(self.lib.ref_load_model(str(manifest).encode(), n, d, None, C.byref(vmin),
+                                            C.byref(vmax)))
+        vp = np.zeros(ghosted_shape(tuple(n), radius), np.float32)
+        self._check(self.lib.ref_load_model(str(manifest).encode(), n, d, _f32(vp),
+                                            C.byref(vmin), C.byref(vmax)))
+        return tuple(n), tuple(d), vp, vmin.value, vmax.value
+
+    def render_report(self, *, ngrid, dgrid, nsteps, fmax, cfl, radius, ndamping, ntaper,
+                      source_loc, receiver_increment, source_increment, nshots, time_rec,
+                      nthreads, vmin, vmax, kernel_s, modeling_s):
+        """render_parameter_block + render_timing (driver.cpp:150-215)."""
+        self._ref_only()
+        buf = C.create_string_buffer(1 << 14)
+        self.lib.ref_render_report.argtypes = None
+        self._check(self.lib.ref_render_report(
+            _i3(*ngrid), _d3(*dgrid), C.c_int(nsteps), C.c_double(fmax), C.c_double(cfl),
+            C.c_int(radius), _i3(*ndamping), _i3(*ntaper),
+            _i3(*source_loc) if source_loc is not None else None,
+            (C.c_int * 2)(*receiver_increment), _i3(*source_increment), C.c_int(nshots),
+            C.c_double(time_rec), C.c_int(nthreads), C.c_float(vmin), C.c_float(vmax),
+            C.c_double(kernel_s), C.c_double(modeling_s), buf, C.c_int(len(buf))))
+        return buf.value.decode()
+
     # ---- engine ---------------------------------------------------------
     def engine(self, n_local, vp_local, *, d=(20.0, 20.0, 20.0), radius=4, offset=(0, 0, 0),
                global_n=None, ndamping=(0, 0, 0), fmax=25.0, r_target=1e-3,

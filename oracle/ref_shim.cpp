@@ -13,6 +13,8 @@
 #include <string>
 
 #include "minimod/driver.hpp"
+#include "minimod/model.hpp"
+#include "minimod/source.hpp"
 #include "minimod/propagator.hpp"
 
 using namespace minimod;
@@ -228,6 +230,94 @@ int ref_taper_material(float* f, const int n[3], int radius, const int ntaper[3]
                                {offset[0], offset[1], offset[2]},
                                {global_n[0], global_n[1], global_n[2]});
         std::memcpy(f, fld.data.data(), sizeof(float) * fld.data.size());
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+// ---- on-disk formats and the report (driver.cpp:150-215, source.cpp:68-95,
+//      model.cpp:80-190): used to pin the repo's writers / parsers byte-wise.
+int ref_save_record(const float* traces, int nrec, int nsteps, double dt, const int source_loc[3],
+                    const int receiver_increment[2], int nshots, const char* path) {
+    try {
+        AcquisitionGeometry g;
+        g.source_loc = {source_loc[0], source_loc[1], source_loc[2]};
+        g.receiver_increment = {receiver_increment[0], receiver_increment[1]};
+        g.nshots = nshots;
+        g.receivers.assign(static_cast<std::size_t>(nrec), std::array<int, 3>{0, 0, 0});
+        ShotRecord r = make_record(g, nsteps, dt);
+        std::memcpy(r.traces.data(), traces, sizeof(float) * r.traces.size());
+        save_record(r, path);
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+// vp: ghosted z-fastest field of a grid with stencil radius `radius`
+int ref_save_model(const int n[3], const double d[3], int radius, const float* vp,
+                   const char* manifest) {
+    try {
+        const EarthModel m = make_model(n, d, radius, vp);
+        save_model(m, manifest);
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+// n, d of the manifest; vp (optional) receives the ghosted field of radius 4
+// (make_grid's default), vmin / vmax as validate_model computed them
+int ref_load_model(const char* manifest, int n[3], double d[3], float* vp, float* vmin,
+                   float* vmax) {
+    try {
+        const EarthModel m = load_model(manifest);
+        for (int a = 0; a < 3; ++a) {
+            n[a] = m.grid.n[a];
+            d[a] = m.grid.d[a];
+        }
+        if (vp) std::memcpy(vp, m.vp.data.data(), sizeof(float) * m.vp.data.size());
+        *vmin = m.vmin;
+        *vmax = m.vmax;
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+int ref_render_report(const int ngrid[3], const double dgrid[3], int nsteps, double fmax,
+                      double cfl, int radius, const int ndamping[3], const int ntaper[3],
+                      const int* source_loc, const int receiver_increment[2],
+                      const int source_increment[3], int nshots, double time_rec, int nthreads,
+                      float vmin, float vmax, double kernel_s, double modeling_s, char* out,
+                      int cap) {
+    try {
+        SimConfig c;
+        c.ngrid = {ngrid[0], ngrid[1], ngrid[2]};
+        c.dgrid = {dgrid[0], dgrid[1], dgrid[2]};
+        c.nsteps = nsteps;
+        c.fmax = fmax;
+        c.cfl = cfl;
+        c.stencil_radius = radius;
+        c.ndamping = {ndamping[0], ndamping[1], ndamping[2]};
+        c.ntaper = {ntaper[0], ntaper[1], ntaper[2]};
+        if (source_loc) c.source_loc = std::array<int, 3>{source_loc[0], source_loc[1], source_loc[2]};
+        c.receiver_increment = {receiver_increment[0], receiver_increment[1]};
+        c.source_increment = {source_increment[0], source_increment[1], source_increment[2]};
+        c.nshots = nshots;
+        c.time_rec = time_rec;
+        c.target = nthreads > 1 ? Target::Parallel : Target::Seq;
+        c.nthreads = nthreads > 1 ? nthreads : 1;
+        EarthModel m;
+        m.vmin = vmin;
+        m.vmax = vmax;
+        RunReport rep;
+        rep.kernel_seconds = kernel_s;
+        rep.modeling_seconds = modeling_s;
+        const std::string s = render_parameter_block(c, m) + render_timing(rep);
+        if ((int)s.size() + 1 > cap) throw std::invalid_argument("report buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
         return 0;
     } catch (...) {
         return catch_all();

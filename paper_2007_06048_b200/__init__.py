@@ -7,7 +7,8 @@ Python front-end over the C-ABI CUDA library ``libminimod_b200.so``
 """
 from ._lib import (CollectiveError, ConfigError, CudaError, InstabilityError, MinimodError,
                    ValidationError, device_count, kernel_launch_count)
-from .driver import RunReport, SimConfig, build_geometry, cfl_dt, run
+from .driver import (RunReport, SimConfig, build_geometry, cfl_dt, render_parameter_block,
+                     render_timing, run)
 from .numerics import (AcquisitionGeometry, AxisCpml, CpmlProfile, EarthModel, Grid3D, IndexBox,
                        RegionPartition, ShotRecord, StencilCoeffs, Wavelet, build_profile,
                        central_first_derivative_coeffs, constant_model, default_layered_model,
@@ -15,6 +16,7 @@ from .numerics import (AcquisitionGeometry, AxisCpml, CpmlProfile, EarthModel, G
                        partition_regions, random_model, ricker, second_derivative_coeffs,
                        taper_material, validate_model, version)
 from .propagator import AcousticCdEngine, EngineOptions
+from .shotio import load_model, load_record, save_model, save_record
 
 __all__ = [
     "AcousticCdEngine", "EngineOptions", "SimConfig", "RunReport", "run", "cfl_dt",
@@ -25,4 +27,6 @@ __all__ = [
     "random_model", "Wavelet", "ricker", "AcquisitionGeometry", "default_receivers",
     "ShotRecord", "ConfigError", "ValidationError", "InstabilityError", "CudaError",
     "CollectiveError", "MinimodError", "device_count", "kernel_launch_count", "version",
+    "render_parameter_block", "render_timing", "save_record", "load_record", "save_model",
+    "load_model",
 ]

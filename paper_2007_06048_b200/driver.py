@@ -104,3 +104,50 @@ def run(config: SimConfig, model: EarthModel, *, device: int = 0,
                        traces.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rep)))
     record = ShotRecord(config.nsteps, rep.dt, geom, traces)
     return record, RunReport(rep.dt, rep.kernel_seconds, rep.modeling_seconds, rep.steps_run)
+
+
+# ------------------------------------------------------------------ report
+# ref: driver.cpp:150-215 -- the Fortran-list-directed parameter block and the
+# timing lines printed by `minimod model`.
+def _f32_repr(v: float) -> str:
+    return "%#.9g" % float(np.float32(v))
+
+
+def _int_row(name: str, vals) -> str:
+    return " %-18s =" % name + "".join("%13d" % int(v) for v in vals) + "\n"
+
+
+def _float_row(name: str, vals) -> str:
+    s = " %-18s =" % name
+    for i, v in enumerate(vals):
+        s += ("    " if i == 0 else "       ") + _f32_repr(v)
+    return s + "    \n"
+
+
+def render_parameter_block(config: SimConfig, model: EarthModel, nthreads: int = 1,
+                           nshots: int = 1, time_rec: float = 0.0,
+                           source_increment=(1, 1, 0)) -> str:
+    """ref: driver.cpp:183-209 render_parameter_block."""
+    grid = make_grid(config.ngrid, config.dgrid, config.stencil_radius)
+    g = build_geometry(config, grid)
+    r = config.stencil_radius
+    return "".join([
+        _int_row("nthreads", [nthreads]), " \n",
+        _int_row("ngrid", config.ngrid), _float_row("dgrid", config.dgrid),
+        _int_row("nsteps", [config.nsteps]), _float_row("fmax", [config.fmax]),
+        _float_row("vmin", [model.vmin]), _float_row("vmax", [model.vmax]),
+        _float_row("cfl", [config.cfl]), " \n",
+        _int_row("stencil", [r, r, r]), _int_row("source_loc", g.source_loc),
+        _int_row("ndamping", config.ndamping), _int_row("ntaper", config.ntaper), " \n",
+        _int_row("nshots", [nshots]), _float_row("time_rec", [time_rec]),
+        _int_row("nreceivers", [g.nreceivers()]),
+        _int_row("receiver_increment", g.receiver_increment),
+        _int_row("source_increment", source_increment), " \n",
+    ])
+
+
+def render_timing(report: RunReport) -> str:
+    """ref: driver.cpp:211-215 render_timing."""
+    return "Time Kernel    %10.2f\nTime Modeling  %10.2f\n" % (report.kernel_seconds,
+                                                              report.modeling_seconds)
+

@@ -88,3 +88,27 @@ def test_device_loop_equals_host_loop(mm):
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
     assert np.array_equal(out[1][0], g["p_cur"])
+
+
+def test_cli_model_shot_record_matches_reference(mm, tmp_path, oracle_ref):
+    """`python -m paper_2007_06048_b200 model` (tools/cli.cpp:264-272): the
+    parameter block, the run and the shot record in the reference's format --
+    traces bit-identical to the reference's own run() of the same command."""
+    import io
+    from paper_2007_06048_b200 import driver, shotio
+    from paper_2007_06048_b200.__main__ import main as cli_main
+    n, nsteps = (64, 60, 62), 20
+    out, err = io.StringIO(), io.StringIO()
+    argv = ["model", "--ngrid", ",".join(map(str, n)), "--nsteps", str(nsteps),
+            "--output", str(tmp_path / "shot.bin")]
+    assert cli_main(argv, out, err) == 0, err.getvalue()
+    cfg = mm.SimConfig(ngrid=n, nsteps=nsteps)
+    model = mm.default_layered_model(mm.make_grid(n, cfg.dgrid))
+    text = out.getvalue()
+    assert text.startswith(driver.render_parameter_block(cfg, model))
+    assert "Time Kernel" in text and "Time Modeling" in text
+    rec = shotio.load_record(tmp_path / "shot.bin")
+    vp, _, _ = oracle_ref.layered_model(n)
+    ref = oracle_ref.run(n, vp, nsteps=nsteps, nthreads=8)
+    assert rec.dt == ref["dt"] and rec.nsteps == nsteps
+    assert np.array_equal(rec.traces, ref["traces"])
