@@ -207,12 +207,15 @@ class ZSlabRank:
     def _view(self, side, which, next_field):
         import torch
         ptr, nbytes = self.e.halo_planes(side, which, next_field=next_field)
+        key = (ptr, nbytes)
+        v = self._views.get(key)  # the 3 rotating buffers give a few fixed views
+        if v is None:
+            class _A:
+                __cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<f4",
+                                            "data": (ptr, False), "version": 3}
 
-        class _A:
-            __cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<f4",
-                                        "data": (ptr, False), "version": 3}
-
-        return torch.as_tensor(_A(), device=f"cuda:{self.e.device}")
+            v = self._views[key] = torch.as_tensor(_A(), device=f"cuda:{self.e.device}")
+        return v
 
     def exchange_current(self):
         """Reference order: exchange p_cur ghosts (dist.cpp:213-214)."""
@@ -377,11 +380,16 @@ def run_zslab(mm, config, vp_global: np.ndarray, info: SlabInfo, transport, *, d
 
 # --------------------------------------------------------------- bench (torchrun)
 def bench_rank(args, rank, world, local):
-    """bench.py --gpus N under torchrun: weak scaling, per-rank 240^3 work:
-    global grid 240 x 240 x (240 N), cost-weighted z slabs, NCCL halos."""
+    """bench.py --gpus N under torchrun: weak scaling, per-rank 240^3 work
+    (global grid 240 x 240 x (240 N)), cost-weighted z slabs, NCCL halos
+    overlapped with the interior.  `value`: device time of K steps of the
+    overlap schedule (max over ranks); `e2e`: the same K steps with the source
+    sample H2D and the receiver plane D2H (rank 0) every step, wall clock, max
+    over ranks."""
     import torch
     import torch.distributed as dist
     import paper_2007_06048_b200 as mm
+    from . import _lib
     from .driver import SimConfig
 
     torch.cuda.set_device(local)
@@ -389,43 +397,84 @@ def bench_rank(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     edge = args.grid or 240
     n = (edge, edge, edge * world)
-    cfg = SimConfig(ngrid=n, nsteps=args.warmup + args.steps, stencil_radius=args.radius)
+    cfg = SimConfig(ngrid=n, nsteps=args.warmup, stencil_radius=args.radius)
     cuts = weighted_cuts(n, cfg.ndamping, args.radius, world)
     info = SlabInfo(rank, world, cuts)
     grid = mm.make_grid(n, cfg.dgrid, args.radius)
     vp = mm.default_layered_model(grid).vp
     tr = TorchTransport()
-    # warm-up then timed, on the same engine: run_zslab does both phases
+    # W warm-up steps (engine, receivers, work lists, NCCL communicators)
     res = run_zslab(mm, cfg, vp, info, tr, device=local, mode=args.mode)
-    # device time of the timed K steps only: rerun K steps timed
     eng = res["engine"]
     rk = ZSlabRank(eng, info, tr, tuple(x // 2 for x in n))
-    w = mm.ricker(cfg.fmax, res["dt"], args.steps).samples
+    w = mm.ricker(cfg.fmax, res["dt"], args.warmup + args.steps).samples[args.warmup:]
     ext = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
-    tr.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(ext)
-    for s in range(args.steps):
-        rk.step_overlap(float(w[s]))
-    e1.record(ext)
-    torch.cuda.synchronize()
-    tr.barrier()
-    ms = tr.max(e0.elapsed_time(e1))
+
+    def timed(e2e: bool):
+        owns = res["owns_receivers"]
+        nrec = n[0] * n[1]
+        host = (torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
+                if e2e and owns else None)
+        if owns:
+            eng.set_receivers(_receivers_local(mm, grid, cfg, info), args.steps)
+        tr.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        l0 = _lib.kernel_launch_count()
+        t0 = time.perf_counter()
+        e0.record(ext)
+        for s in range(args.steps):
+            rk.step_overlap(float(w[s]))
+            if owns:
+                eng.record(s)
+                if e2e:
+                    eng.copy_trace_step(s, host[s], asynchronous=True)
+        e1.record(ext)
+        eng.synchronize()
+        wall = time.perf_counter() - t0
+        launches = _lib.kernel_launch_count() - l0
+        torch.cuda.synchronize()
+        tr.barrier()
+        return e0.elapsed_time(e1), wall * 1e3, launches, (nrec * 4 if owns else 0)
+
+    from .clocks import ClockSampler
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, _, launches, _ = timed(False)
+    clk = clocks.stop()
+    dev_ms = tr.max(ms)
+    _, wall_ms, _, d2h = timed(True)
+    e2e_ms = tr.max(max(wall_ms, ms))
+    d2h = int(tr.max(float(d2h)))
     pts = float(n[0]) * n[1] * n[2]
-    value = pts * args.steps / (ms * 1e-3) / 1e9
+    value = pts * args.steps / (dev_ms * 1e-3) / 1e9
+    e2e = pts * args.steps / (e2e_ms * 1e-3) / 1e9
+    all_launches = int(tr.max(float(launches)) * world) if world > 1 else launches
     if rank == 0:
         print(json.dumps({
             "metric": "Gpoints/s (grid-point updates/sec) acoustic_iso_cd 8th-order",
             "value": round(value, 3), "unit": "Gpoints/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (default two-layer vp model)",
-            "config": {"workload": f"acoustic_iso_cd r={args.radius} {n[0]}x{n[1]}x{n[2]} grid "
-                                   f"z-slabs {cuts}, NCCL halo exchange overlapped",
-                       "grid": list(n), "cuts": cuts,
-                       "balance": round(balance(n, cfg.ndamping, cuts), 4)},
+            "data": "synthetic (default two-layer vp model 1500/4500, Ricker source)",
+            "config": {"workload": f"acoustic_iso_cd r={args.radius} {n[0]}x{n[1]}x{n[2]} grid, "
+                                   f"z-slabs {cuts}, NCCL halo exchange overlapped "
+                                   "with the interior (weak scaling: 240^3 per GPU)",
+                       "grid": list(n), "cuts": cuts, "radius": args.radius,
+                       "balance": round(balance(n, cfg.ndamping, cuts), 4), "mode": args.mode,
+                       "l2": "working set > 126 MB L2 per GPU; no flush"},
+            "e2e": {"value": round(e2e, 3), "unit": "Gpoints/s", "h2d_bytes_per_step": 4 * world,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": all_launches,
+            "clocks": clk,
         }), flush=True)
     dist.destroy_process_group()
     return 0
+
+
+def _receivers_local(mm, grid, cfg, info):
+    geo = mm.default_receivers(grid, cfg.ndamping, cfg.receiver_increment)
+    rec = geo.receivers.copy()
+    rec[:, 2] -= info.z0
+    return rec
