@@ -29,6 +29,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#ifndef MM_PROD_SLEEP_NS
+#define MM_PROD_SLEEP_NS 64
+#endif
 // Producer-side wait: back off with nanosleep between polls so a spinning
 // producer lane does not take issue slots from the consumer warps.
 __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
@@ -59,7 +62,11 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
-    while (!mbar_try(bar, parity)) __nanosleep(64);
+#ifdef MM_PROD_SPIN
+    mbar_wait(bar, parity);
+#else
+    while (!mbar_try(bar, parity)) __nanosleep(MM_PROD_SLEEP_NS);
+#endif
 }
 __device__ __forceinline__ void mbar_arrive_b(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");

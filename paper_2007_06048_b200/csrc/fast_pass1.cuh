@@ -20,8 +20,13 @@ namespace fast {
 #ifndef MM_P1_LEAD
 #define MM_P1_LEAD 4
 #endif
+#ifndef MM_P1_NQ
+#define MM_P1_NQ 8
+#endif
 
-template <int R>
+// Z = true: the z-run items (2R+1-plane window, dpsi_z emission); Z = false:
+// the x- and y-run items, which need no window and run many more CTAs per SM.
+template <int R, bool Z>
 struct P1Cfg {
     static constexpr int TX = 32, TY = 16;
     static constexpr int NC = (TX / 4) * TY;  // 128 consumer threads, float4 each
@@ -33,14 +38,13 @@ struct P1Cfg {
     static constexpr int PXN = BXX * TY, PYN = TX * BYY, PZN = TX * TY;
     static constexpr int PSLOT = pad32(PXN > PYN ? PXN : PYN);
     static constexpr int PSI_N = TX * TY, PSI = pad32(PSI_N);
-    static constexpr int D = MM_P1_LEAD;      // producer lead beyond the z window
-    static constexpr int NS = 2 * R + 1 + D;  // p slots
-    static constexpr int NQ = MM_P1_LEAD;     // psi stages
+    static constexpr int D = Z ? MM_P1_LEAD : 6;  // producer lead beyond the z window
+    static constexpr int NS = (Z ? 2 * R + 1 : 1) + D;  // p slots
+    static constexpr int NQ = Z ? MM_P1_NQ : 8;   // psi stages
     static constexpr int QLEAD = NQ - 1;
-    static constexpr int QW = 2 * R + 1;      // window of new psi_z planes
     static constexpr int NBAR = 2 * NS + 2 * NQ + 4;
     static constexpr size_t SMEM =
-        sizeof(float) * (size_t)(NS * PSLOT + NQ * PSI + QW * PSI) + 8 * NBAR + 64;
+        sizeof(float) * (size_t)(NS * PSLOT + NQ * PSI) + 8 * NBAR + 64;
 };
 
 struct P1Maps {
@@ -69,32 +73,31 @@ struct P1Params {
     float* dpz[2];
 };
 
-template <int R>
+template <int R, bool Z>
 struct P1Tile {
     int ax, side, x0, y0, zb, ze, w, nring, nout;
     __device__ P1Tile(const P1Params& P, const int4& sg) {
         const RunDesc& d = P.rd[sg.x & 7];
         ax = d.ax;
         side = d.side;
-        x0 = d.x_base + (sg.x >> 3) * P1Cfg<R>::TX;
-        y0 = d.lo[1] + sg.y * P1Cfg<R>::TY;
+        x0 = d.x_base + (sg.x >> 3) * P1Cfg<R, Z>::TX;
+        y0 = d.lo[1] + sg.y * P1Cfg<R, Z>::TY;
         zb = sg.z;
         ze = sg.w;
-        w = ax == 2 ? R : 0;  // z window half-width
+        w = Z && ax == 2 ? R : 0;  // z window half-width
         nout = ze - zb;
         nring = nout + 2 * w;
     }
 };
 
-template <int R, int ORD>
-__global__ void __launch_bounds__(P1Cfg<R>::NT)
+template <int R, int ORD, bool Z>
+__global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
     k_p1(const __grid_constant__ P1Maps M, const P1Params P) {
-    using C = P1Cfg<R>;
+    using C = P1Cfg<R, Z>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
     float* qring = ring + C::NS * C::PSLOT;
-    float* zwin = qring + C::NQ * C::PSI;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(zwin + C::QW * C::PSI);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(qring + C::NQ * C::PSI);
     int4* items = reinterpret_cast<int4*>(bars + C::NBAR);
     const uint32_t fullP = smem_u32(bars), emptyP = fullP + 8 * C::NS;
     const uint32_t fullQ = emptyP + 8 * C::NS, emptyQ = fullQ + 8 * C::NQ;
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(P1Cfg<R>::NT)
                     ++ni;
                 }
                 if (sg.w < 0) break;
-                const P1Tile<R> T(P, sg);
+                const P1Tile<R, Z> T(P, sg);
                 const CpmlRun& run = P.run[T.ax][T.side];
                 const CUtensorMap* pmap = T.ax == 0 ? &M.px : T.ax == 1 ? &M.py : &M.pz;
                 const uint32_t pbytes = 4u * (T.ax == 0 ? C::PXN : T.ax == 1 ? C::PYN : C::PZN);
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(P1Cfg<R>::NT)
             ++ni;
         }
         if (sg.w < 0) break;
-        const P1Tile<R> T(P, sg);
+        const P1Tile<R, Z> T(P, sg);
         const int ax = T.ax;
         const RunDesc& d = P.rd[sg.x & 7];
         const CpmlRun& run = P.run[ax][T.side];
@@ -240,24 +243,92 @@ __global__ void __launch_bounds__(P1Cfg<R>::NT)
                 if (ok[3]) q[3] = v.w;
             }
         };
-        // z runs (items cover the whole run, zb = lo, ze = hi): dpsi_z at plane
-        // zb + od for od = -R .. nout+R-1, from the new psi_z window
-        auto emit_dpz = [&](int od) {
-            float dz[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (Z) {
+            // z runs (an item covers the whole run, zb = lo, ze = hi).  The
+            // new psi_z of this thread's points rides a register queue
+            // zq[k] = plane o-2R+k (zeros outside the run), from which dpsi_z
+            // at plane od = o-R is emitted as soon as plane o is done; the
+            // p_cur z window is addressed through rotating slot offsets.
+            float4 zq[2 * R + 1];
 #pragma unroll
-            for (int m = 1; m <= R; ++m) {
-                const int a = od + m, b = od - m;
-                const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-                const float4 u4 = a >= 0 && a < T.nout ? lds4(zwin + (a % C::QW) * C::PSI + qoff) : zero;
-                const float4 d4 = b >= 0 && b < T.nout ? lds4(zwin + (b % C::QW) * C::PSI + qoff) : zero;
-                dz[0] = acc<ORD>(dz[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
-                dz[1] = acc<ORD>(dz[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
-                dz[2] = acc<ORD>(dz[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
-                dz[3] = acc<ORD>(dz[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
+            for (int k = 0; k <= 2 * R; ++k) zq[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            float* dz_p = P.dpz[T.side] + x + (long long)y * run.s1;  // plane od = -R
+            auto emit_dpz = [&]() {  // dpsi_z at queue centre (plane od)
+                float dz[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int m = 1; m <= R; ++m) {
+                    const float4 u4 = zq[R + m], d4 = zq[R - m];
+                    dz[0] = acc<ORD>(dz[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
+                    dz[1] = acc<ORD>(dz[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
+                    dz[2] = acc<ORD>(dz[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
+                    dz[3] = acc<ORD>(dz[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
+                }
+                store4(dz_p, make_float4(dz[0], dz[1], dz[2], dz[3]));
+                dz_p += run.s2;
+            };
+            int wo[2 * R + 1];     // p_cur slot offsets of planes j-2R .. j
+            int rel = (int)(np % C::NS);  // slot of the oldest window plane
+            int sl = rel;                 // slot of plane j
+            unsigned ph = (np / C::NS) & 1;
+#pragma unroll 1
+            for (int j = 0; j < T.nring; ++j) {
+#pragma unroll
+                for (int k = 0; k < 2 * R; ++k) wo[k] = wo[k + 1];
+                wo[2 * R] = sl * C::PSLOT + poff;
+                mbar_wait(fullP + 8 * sl, ph);
+                if (j >= 2 * R) {
+                    const int o = j - 2 * R;
+                    const int z = T.zb + o;
+                    const float az = __ldg(P.ta[2] + z), bz = __ldg(P.tb[2] + z);
+                    float dp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int m = 1; m <= R; ++m) {
+                        const float4 u4 = lds4(ring + wo[R + m]), d4 = lds4(ring + wo[R - m]);
+                        dp[0] = acc<ORD>(dp[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
+                        dp[1] = acc<ORD>(dp[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
+                        dp[2] = acc<ORD>(dp[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
+                        dp[3] = acc<ORD>(dp[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
+                    }
+                    const int st = nq % C::NQ;
+                    mbar_wait(fullQ + 8 * st, (nq / C::NQ) & 1);
+                    float4 v = lds4(qring + st * C::PSI + qoff);
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive_b(emptyQ + 8 * st);
+                        mbar_arrive_b(emptyP + 8 * rel);  // plane j - 2R has had its last use
+                    }
+                    ++nq;
+                    if (++rel == C::NS) rel = 0;
+                    // reference: psi = b * psi + a * dp  (propagator_impl.hpp:118-120)
+                    v.x = acc<ORD>(fm<ORD>(az, dp[0]), bz, v.x);
+                    v.y = acc<ORD>(fm<ORD>(az, dp[1]), bz, v.y);
+                    v.z = acc<ORD>(fm<ORD>(az, dp[2]), bz, v.z);
+                    v.w = acc<ORD>(fm<ORD>(az, dp[3]), bz, v.w);
+                    store4(dst + (long long)o * zstep, v);
+#pragma unroll
+                    for (int k = 0; k < 2 * R; ++k) zq[k] = zq[k + 1];
+                    zq[2 * R] = v;
+                    emit_dpz();  // plane o - R: its window ends at plane o
+                }
+                ++np;
+                if (++sl == C::NS) sl = 0, ph ^= 1;
             }
-            store4(P.dpz[T.side] + x + (long long)y * run.s1 + (long long)(od + R) * run.s2,
-                   make_float4(dz[0], dz[1], dz[2], dz[3]));
-        };
+            // planes whose window reaches past the run: psi_z = 0 there
+#pragma unroll 1
+            for (int t = 0; t < 2 * R; ++t) {
+#pragma unroll
+                for (int k = 0; k < 2 * R; ++k) zq[k] = zq[k + 1];
+                zq[2 * R] = make_float4(0.f, 0.f, 0.f, 0.f);
+                emit_dpz();
+            }
+#pragma unroll 1
+            for (int k = 0; k < 2 * R; ++k) {  // the item's last 2R planes
+                __syncwarp();
+                if (lane == 0) mbar_arrive_b(emptyP + 8 * rel);
+                if (++rel == C::NS) rel = 0;
+            }
+            continue;
+        }
 #pragma unroll 1
         for (int j = 0; j < T.nring; ++j) {
             const int s = np % C::NS;
@@ -324,16 +395,9 @@ __global__ void __launch_bounds__(P1Cfg<R>::NT)
                 // plane j - 2w has had its last use
                 __syncwarp();
                 if (lane == 0) mbar_arrive_b(emptyP + 8 * slot_of(-T.w));
-                if (ax == 2) {
-                    // this thread's window of new psi_z (no other thread reads it)
-                    *reinterpret_cast<float4*>(zwin + (o % C::QW) * C::PSI + qoff) = v;
-                    emit_dpz(o - R);  // its window ends at plane o
-                }
             }
             ++np;
         }
-        if (ax == 2)  // planes whose window reaches past the run: psi_z = 0 there
-            for (int od = T.nout - R; od < T.nout + R; ++od) emit_dpz(od);
 #pragma unroll 1
         for (int k = 2 * T.w; k >= 1; --k) {  // the item's last 2w planes
             __syncwarp();

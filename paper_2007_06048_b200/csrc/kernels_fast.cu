@@ -154,7 +154,8 @@ template <int R>
 class FastPlanR final : public FastPlan {
     using IC = InnerCfg<R>;
     using BC = BndCfg<R>;
-    using P1C = P1Cfg<R>;
+    using P1C = P1Cfg<R, true>;    // z runs (dpsi_z window)
+    using P1X = P1Cfg<R, false>;   // x and y runs
     static constexpr bool kBnd = BC::SMEM <= 227 * 1024;  // TMA boundary kernel fits
     static constexpr bool kZs = ZSlabCfg<R>::SMEM <= 227 * 1024;  // optional Z-slab kernel
     static constexpr bool kP1 = P1C::SMEM <= 200 * 1024;
@@ -190,8 +191,17 @@ public:
         if (const char* zm = std::getenv("MM_ZSLABS")) zmode_ = std::max(0, std::min(2, std::atoi(zm)));
         if (!kZs) zmode_ = 0;
         { const char* ov = std::getenv("MM_OVERLAP"); overlap_ = !ov || ov[0] != '0'; }
+        // stream priorities: the z-run pass 1 (the step's critical path) is
+        // scheduled before the interior kernel of the side branch
+        int prio_lo = 0, prio_hi = 0;
+        MM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        MM_CUDA(cudaStreamCreateWithPriority(&p1_side_, cudaStreamNonBlocking, prio_hi));
+        MM_CUDA(cudaEventCreateWithFlags(&p1_fork_, cudaEventDisableTiming));
+        MM_CUDA(cudaEventCreateWithFlags(&p1_join_, cudaEventDisableTiming));
         if (overlap_) {
-            MM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+            int lo = 0, hi = 0;
+            MM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            MM_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, lo));
             MM_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
             MM_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
         }
@@ -224,19 +234,27 @@ public:
             bnd_per_sm_ = std::max(1, per_sm);
         }
         if constexpr (kP1) {
-            MM_CUDA(cudaFuncSetAttribute(k_p1<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)P1C::SMEM));
-            MM_CUDA(cudaFuncSetAttribute(k_p1<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)P1C::SMEM));
-            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p1<R, 2>, P1C::NT,
-                                                                  P1C::SMEM));
+            for (auto fn : {k_p1<R, 1, true>, k_p1<R, 2, true>})
+                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)P1C::SMEM));
+            for (auto fn : {k_p1<R, 1, false>, k_p1<R, 2, false>})
+                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)P1X::SMEM));
+            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p1<R, 2, true>,
+                                                                  P1C::NT, P1C::SMEM));
             p1_per_sm_ = std::max(1, per_sm);
+            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p1<R, 2, false>,
+                                                                  P1X::NT, P1X::SMEM));
+            p1x_per_sm_ = std::max(1, per_sm);
         }
     }
     ~FastPlanR() override {
         if (fork_) cudaEventDestroy(fork_);
         if (join_) cudaEventDestroy(join_);
         if (side_) cudaStreamDestroy(side_);
+        if (p1_fork_) cudaEventDestroy(p1_fork_);
+        if (p1_join_) cudaEventDestroy(p1_join_);
+        if (p1_side_) cudaStreamDestroy(p1_side_);
     }
 
     void pass1(const StepParams& p, cudaStream_t s) override { launch_pass1(p, 0, lay_.n[2], s); }
@@ -626,13 +644,17 @@ private:
                                     tiles.push_back(Item{ri | (a << 3), b, d.lo[2], d.hi[2]});
                             }
                     }
+                // two launches: the x/y runs (many small CTAs) and the z runs
                 std::vector<int4> items;
-                wave_items(tiles, sms_ * p1_per_sm_, p1_zt_, items);
-                items.insert(items.begin(), zitems.begin(), zitems.end());  // longest first
+                wave_items(tiles, sms_ * p1x_per_sm_, p1_zt_, items);
+                e.nx = (int)items.size();
+                e.ctas_x = std::max(1, std::min(sms_ * p1x_per_sm_, e.nx));
+                e.nz = (int)zitems.size();
+                e.ctas_z = std::max(1, std::min(sms_ * p1_per_sm_, e.nz));
+                items.insert(items.end(), zitems.begin(), zitems.end());
                 e.nitems = (int)items.size();
-                e.ctas = std::max(1, std::min(sms_ * p1_per_sm_, e.nitems));
                 e.items.set(items, stream_setup_);
-                e.ctr.set(std::vector<int>{0, 0}, stream_setup_);
+                e.ctr.set(std::vector<int>{0, 0, 0, 0}, stream_setup_);
                 it = pass1_cache_.find(key);
             }
             auto& e = it->second;
@@ -653,26 +675,51 @@ private:
                 pp.tb[a] = p.tb[a];
                 for (int m = 0; m < kMaxR; ++m) pp.c1[a][m] = p.c1[a][m];
             }
-            pp.items = e.items.ptr;
-            pp.wq = WorkQueue{e.ctr.ptr, e.nitems};
             pp.dpz[0] = dpz_[0].ptr;
             pp.dpz[1] = dpz_[1].ptr;
-            if (order_ == 2)
-                k_p1<R, 2><<<e.ctas, P1C::NT, P1C::SMEM, s>>>(p1maps_, pp);
-            else
-                k_p1<R, 1><<<e.ctas, P1C::NT, P1C::SMEM, s>>>(p1maps_, pp);
-            note_launches(1);
-            MM_CUDA(cudaGetLastError());
+            // the two launches run concurrently (z on a second stream, joined
+            // before returning): the long z items share the SMs with x/y work
+            const bool two = e.nz > 0 && e.nx > 0 && p1_side_;
+            cudaStream_t sz = s;
+            if (two) {
+                MM_CUDA(cudaEventRecord(p1_fork_, s));
+                MM_CUDA(cudaStreamWaitEvent(p1_side_, p1_fork_, 0));
+                sz = p1_side_;
+            }
+            if (e.nz > 0) {  // z runs first: their items are the long ones
+                pp.items = e.items.ptr + e.nx;
+                pp.wq = WorkQueue{e.ctr.ptr + 2, e.nz};
+                if (order_ == 2)
+                    k_p1<R, 2, true><<<e.ctas_z, P1C::NT, P1C::SMEM, sz>>>(p1maps_, pp);
+                else
+                    k_p1<R, 1, true><<<e.ctas_z, P1C::NT, P1C::SMEM, sz>>>(p1maps_, pp);
+                note_launches(1);
+                MM_CUDA(cudaGetLastError());
+            }
+            if (e.nx > 0) {
+                pp.items = e.items.ptr;
+                pp.wq = WorkQueue{e.ctr.ptr, e.nx};
+                if (order_ == 2)
+                    k_p1<R, 2, false><<<e.ctas_x, P1X::NT, P1X::SMEM, s>>>(p1maps_, pp);
+                else
+                    k_p1<R, 1, false><<<e.ctas_x, P1X::NT, P1X::SMEM, s>>>(p1maps_, pp);
+                note_launches(1);
+                MM_CUDA(cudaGetLastError());
+            }
+            if (two) {
+                MM_CUDA(cudaEventRecord(p1_join_, p1_side_));
+                MM_CUDA(cudaStreamWaitEvent(s, p1_join_, 0));
+            }
         }
     }
 
     struct Pass1Work {
         RunDesc rd[6];
         int nrd = 0;
-        DArr<int4> items;
-        DArr<int> ctr;
-        int nitems = 0;
-        int ctas = 0;
+        DArr<int4> items;  // x/y-run items, then z-run items
+        DArr<int> ctr;     // two WorkQueue counter pairs
+        int nitems = 0, nx = 0, nz = 0;
+        int ctas_x = 0, ctas_z = 0;
     };
 
     Layout lay_;
@@ -684,6 +731,8 @@ private:
     bool overlap_ = false;
     cudaStream_t side_ = nullptr;
     cudaEvent_t fork_ = nullptr, join_ = nullptr;
+    cudaStream_t p1_side_ = nullptr;
+    cudaEvent_t p1_fork_ = nullptr, p1_join_ = nullptr;
     bool col_inner_ = false;
     const float* bufs_[3];
     CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;
@@ -693,7 +742,7 @@ private:
     int dz_lo_[2] = {0, 0}, dz_hi_[2] = {0, 0};
     bool dpz_valid_ = false, zmix_ = false;
     CUtensorMap p1x_[3], p1y_[3], p1z_[3];
-    int p1_per_sm_ = 1;
+    int p1_per_sm_ = 1, p1x_per_sm_ = 1;
     double p1_zt_ = 16.0;
     CpmlRun runs_[3][2] = {};
     bool runs_valid_ = false;
