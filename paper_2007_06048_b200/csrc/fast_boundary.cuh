@@ -231,6 +231,9 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                 atomicExch(P.wq.ctr + 1, 0);
             }
         } else if (lane == 1) {
+            // the stages carry pass-1 results (psi, dpsi_z): with a programmatic
+            // launch after k_p1 they wait for it; the p_cur ring (lane 0) does not
+            grid_dep_wait();
             unsigned nq = 0, qtail = 0, ni = 0;
             uint32_t V = 0;
             for (;;) {

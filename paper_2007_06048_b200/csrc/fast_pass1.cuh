@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
     const int warp = tid / 32, lane = tid % 32;
     const Layout L = P.lay;
 
+    // the boundary kernel may be scheduled as soon as SMs free up (it waits
+    // for this grid's results itself)
+    grid_dep_launch();
     if (tid == 0) {
         for (int s = 0; s < C::NS; ++s) {
             mbar_init(fullP + 8 * s, 1);

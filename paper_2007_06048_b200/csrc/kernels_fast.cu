@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "fast_boundary.cuh"
@@ -120,6 +121,25 @@ struct Box {
     int lo[3], hi[3];
 };
 
+// Launch with programmatic dependent launch allowed (PDL): the kernel may start
+// while the previous kernel in the stream drains; it orders its dependent
+// reads itself (griddepcontrol.wait).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                bool pdl, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? at : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    MM_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // Work items for the persistent kernels: each (tile, z-chunk) is one item.
 // Items are ordered chunk-major (all tiles of chunk 0, then chunk 1, ...) and
 // handed out dynamically (WorkQueue), so the items in flight at any moment are
@@ -191,11 +211,13 @@ public:
         if (const char* zm = std::getenv("MM_ZSLABS")) zmode_ = std::max(0, std::min(2, std::atoi(zm)));
         if (!kZs) zmode_ = 0;
         { const char* ov = std::getenv("MM_OVERLAP"); overlap_ = !ov || ov[0] != '0'; }
-        // stream priorities: the z-run pass 1 (the step's critical path) is
-        // scheduled before the interior kernel of the side branch
+        // side streams at the lowest priority: pass 1's z runs (on the step's
+        // stream, the critical path) are scheduled first
         int prio_lo = 0, prio_hi = 0;
         MM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        MM_CUDA(cudaStreamCreateWithPriority(&p1_side_, cudaStreamNonBlocking, prio_hi));
+        MM_CUDA(cudaStreamCreateWithPriority(&p1_side_, cudaStreamNonBlocking, prio_lo));
+        (void)prio_hi;
+        { const char* e = std::getenv("MM_PDL"); pdl_ = !e || e[0] != '0'; }
         MM_CUDA(cudaEventCreateWithFlags(&p1_fork_, cudaEventDisableTiming));
         MM_CUDA(cudaEventCreateWithFlags(&p1_join_, cudaEventDisableTiming));
         if (overlap_) {
@@ -590,9 +612,9 @@ private:
             bp_.segs = w.segs.ptr;
             bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
             if (order_ == 2)
-                k_bnd<R, 2><<<w.ctas, BC::NT, BC::SMEM, s>>>(maps_, bp_);
+                launch_pdl(k_bnd<R, 2>, w.ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
             else
-                k_bnd<R, 1><<<w.ctas, BC::NT, BC::SMEM, s>>>(maps_, bp_);
+                launch_pdl(k_bnd<R, 1>, w.ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
             note_launches(1);
             MM_CUDA(cudaGetLastError());
         }
@@ -679,12 +701,14 @@ private:
             pp.dpz[1] = dpz_[1].ptr;
             // the two launches run concurrently (z on a second stream, joined
             // before returning): the long z items share the SMs with x/y work
+            // (z on the step's stream, so the boundary kernel can follow it with
+            // a programmatic dependency; x/y on a second stream, joined first)
             const bool two = e.nz > 0 && e.nx > 0 && p1_side_;
-            cudaStream_t sz = s;
+            cudaStream_t sz = s, sx = s;
             if (two) {
                 MM_CUDA(cudaEventRecord(p1_fork_, s));
                 MM_CUDA(cudaStreamWaitEvent(p1_side_, p1_fork_, 0));
-                sz = p1_side_;
+                sx = p1_side_;
             }
             if (e.nz > 0) {  // z runs first: their items are the long ones
                 pp.items = e.items.ptr + e.nx;
@@ -700,9 +724,9 @@ private:
                 pp.items = e.items.ptr;
                 pp.wq = WorkQueue{e.ctr.ptr, e.nx};
                 if (order_ == 2)
-                    k_p1<R, 2, false><<<e.ctas_x, P1X::NT, P1X::SMEM, s>>>(p1maps_, pp);
+                    k_p1<R, 2, false><<<e.ctas_x, P1X::NT, P1X::SMEM, sx>>>(p1maps_, pp);
                 else
-                    k_p1<R, 1, false><<<e.ctas_x, P1X::NT, P1X::SMEM, s>>>(p1maps_, pp);
+                    k_p1<R, 1, false><<<e.ctas_x, P1X::NT, P1X::SMEM, sx>>>(p1maps_, pp);
                 note_launches(1);
                 MM_CUDA(cudaGetLastError());
             }
@@ -728,6 +752,7 @@ private:
     int order_ = 2;
     double inner_zt_ = 48.0, bnd_zt_ = 48.0;
     int zmode_ = 0;
+    bool pdl_ = true;
     bool overlap_ = false;
     cudaStream_t side_ = nullptr;
     cudaEvent_t fork_ = nullptr, join_ = nullptr;
