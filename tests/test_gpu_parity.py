@@ -208,6 +208,32 @@ def test_random_model_vs_oracle(mm, oracle_port, mode):
         assert err <= FAST_REL_L2, f"rel L2 {err:.3e}"
 
 
+@pytest.mark.parametrize("n,nd,radius,fs,src", [
+    ((100, 90, 96), (40, 33, 30), 4, False, (50, 45, 48)),   # slabs wider than a tile
+    ((61, 47, 53), (9, 7, 11), 4, True, (30, 23, 40)),       # odd extents, free surface
+    ((70, 66, 58), (13, 0, 12), 2, False, (35, 33, 29)),     # r = 2, no y damping
+    ((52, 56, 60), (6, 9, 7), 8, False, (26, 28, 30)),       # r = 8
+    ((64, 64, 40), (20, 20, 8), 4, False, (32, 32, 20)),     # z runs 2R apart (strict CPML)
+])
+def test_fast_bitwise_equal_strict_odd_configs(mm, n, nd, radius, fs, src):
+    """The fast kernels' tiling, chunking and CPML-run paths on shapes the
+    golden cases do not reach; the strict path is bit-identical to the
+    reference (goldens above), so fast == strict means fast == reference."""
+    steps, dt = 60, 1.0e-3
+    grid = mm.make_grid(n, (20.0, 15.0, 10.0), radius)
+    m = mm.random_model(grid, seed=11)
+    w = mm.ricker(25.0, dt, steps).samples
+    opts = mm.EngineOptions(ndamping=nd, taper=True, free_surface=fs)
+    eng = {md: mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, dt, m.vmax, mode=md)
+           for md in ("fast", "strict")}
+    for s in range(steps):
+        for e in eng.values():
+            e.step(float(w[s]), src)
+    a, b = eng["fast"].pressure(), eng["strict"].pressure()
+    assert np.array_equal(a, b), f"{int(np.count_nonzero(a != b))} points differ"
+    assert np.array_equal(eng["fast"].pressure_prev(), eng["strict"].pressure_prev())
+
+
 def test_two_engine_zslab_halo_exchange_bitwise(mm):
     """Two z-slab engines on one device, halos moved through the C-ABI plane
     pointers, equal the single engine (test_dist.cpp:107-118 restated)."""
