@@ -145,8 +145,11 @@ def cpu_sample_steps(n, requested):
 
 
 # ------------------------------------------------------------------ our arm
-def default_grid(world):
-    return 240 if world == 1 else 512
+def workload_grid(args, world):
+    """BASELINE configs[1] per GPU: 240^3 at N = 1; weak scaling at N > 1 grows
+    z, 240 x 240 x 240 N (the multi-GPU leg in dist.bench_rank uses the same)."""
+    edge = args.grid or 240
+    return (edge, edge, edge * world)
 
 
 def run_ours(args):
@@ -158,8 +161,8 @@ def run_ours(args):
     import paper_2007_06048_b200 as mm
     from paper_2007_06048_b200 import _lib
 
-    edge = args.grid or default_grid(world)
-    n = (edge, edge, edge)
+    n = workload_grid(args, world)
+    edge = n[0]
     r = args.radius
     nd = (27, 27, 27)
     torch.cuda.set_device(local)
@@ -304,8 +307,7 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    edge = args.grid or default_grid(world)
-    n = (edge, edge, edge)
+    n = workload_grid(args, world)
     from oracle.oracle import nproc
     cores = nproc()
     ns = max(1, min(args.steps, cpu_sample_steps(n, args.cpu_sample_steps)))
@@ -317,10 +319,10 @@ def run_reference(args):
         "n_gpus": world, "steps": ns, "warmup": args.warmup,
         "ms_per_step": secs * 1e3 / ns, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (default two-layer model)",
-        "config": {"workload": f"acoustic_iso_cd r=4 {edge}^3 grid, nd=27 CPML, taper "
-                               f"(bounded sample: {ns} steps from t=0)", "grid": list(n)},
+        "config": {"workload": f"acoustic_iso_cd r=4 {n[0]}x{n[1]}x{n[2]} grid, nd=27 CPML, "
+                               f"taper (bounded sample: {ns} steps from t=0)", "grid": list(n)},
         "cpu_baseline": {"value": round(gpts, 5), "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{edge}^3 x {ns} steps, run() Target::Parallel"},
+                         "sample": f"{n[0]}x{n[1]}x{n[2]} x {ns} steps, run() Target::Parallel"},
         "e2e": {"value": round(gpts, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
