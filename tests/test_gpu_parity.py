@@ -234,6 +234,31 @@ def test_fast_bitwise_equal_strict_odd_configs(mm, n, nd, radius, fs, src):
     assert np.array_equal(eng["fast"].pressure_prev(), eng["strict"].pressure_prev())
 
 
+@pytest.mark.slow
+def test_fast_equals_strict_large_random_state(mm):
+    """1000 x 1000 x 200 with random p_prev / p_cur everywhere (every CPML run
+    and slab active from step 0): offsets past 2^32 bytes, 1000-wide tensor
+    maps, many work items; fast == strict bit for bit after a few steps."""
+    n, nd, steps = (1000, 1000, 200), (27, 27, 27), 4
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0))
+    model = mm.default_layered_model(grid)
+    rng = np.random.default_rng(5)
+    p0 = rng.standard_normal(grid.shape, dtype=np.float32)
+    p1 = rng.standard_normal(grid.shape, dtype=np.float32)
+    opts = mm.EngineOptions(ndamping=nd, taper=True)
+    dt = 1.0e-3
+    out = {}
+    for md in ("fast", "strict"):
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax, mode=md)
+        e.set_state(p0, p1)
+        for s in range(steps):
+            e.step(0.5, (500, 500, 100))
+        out[md] = e.pressure()
+        del e
+    a, b = out["fast"], out["strict"]
+    assert np.array_equal(a, b), f"{int(np.count_nonzero(a != b))} points differ"
+
+
 def test_two_engine_zslab_halo_exchange_bitwise(mm):
     """Two z-slab engines on one device, halos moved through the C-ABI plane
     pointers, equal the single engine (test_dist.cpp:107-118 restated)."""
