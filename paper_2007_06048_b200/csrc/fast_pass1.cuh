@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
         if constexpr (Z) {
             // z runs (an item covers the whole run, zb = lo, ze = hi).  The
             // new psi_z of this thread's points rides a register queue
-            // zq[k] = plane o-2R+k (zeros outside the run), from which dpsi_z
-            // at plane od = o-R is emitted as soon as plane o is done; the
+            // zq[k] = plane o-1-2R+k (zeros outside the run), from which dpsi_z
+            // at plane o-1-R is emitted while plane o is computed; the
             // p_cur z window is addressed through rotating slot offsets.
             float4 zq[2 * R + 1];
 #pragma unroll
@@ -282,6 +282,9 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                 if (j >= 2 * R) {
                     const int o = j - 2 * R;
                     const int z = T.zb + o;
+                    // dpsi_z of plane o-1-R first: its window ends at plane o-1, so
+                    // it is independent of this plane's psi (more ILP per plane)
+                    if (o > 0) emit_dpz();
                     const float az = __ldg(P.ta[2] + z), bz = __ldg(P.tb[2] + z);
                     float dp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -311,12 +314,13 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
 #pragma unroll
                     for (int k = 0; k < 2 * R; ++k) zq[k] = zq[k + 1];
                     zq[2 * R] = v;
-                    emit_dpz();  // plane o - R: its window ends at plane o
                 }
                 ++np;
                 if (++sl == C::NS) sl = 0, ph ^= 1;
             }
-            // planes whose window reaches past the run: psi_z = 0 there
+            // the last plane's dpsi_z, then the planes whose window reaches
+            // past the run (psi_z = 0 there)
+            emit_dpz();
 #pragma unroll 1
             for (int t = 0; t < 2 * R; ++t) {
 #pragma unroll
