@@ -193,6 +193,9 @@ int mm_cd_next_halo_planes(mm_cd_engine* e, int side, int which, void** dev_ptr,
 /* Restricted step pieces for overlap: compute p_next on local planes
  * [z_lo, z_hi) only (both CPML passes and the inner update). */
 int mm_cd_update_planes(mm_cd_engine* e, int z_lo, int z_hi);
+/* Same on the union of n plane ranges [ranges[2i], ranges[2i+1]) (e.g. the
+ * edge planes next to both cuts), with one launch per kernel. */
+int mm_cd_update_plane_ranges(mm_cd_engine* e, const int* ranges, int n);
 
 /* ------------------------------------------------------------------------
  * Driver (ref: driver.cpp:83-144 run(), acoustic_iso_cd only)

@@ -130,6 +130,7 @@ SIGNATURES = {
     "mm_cd_halo_planes": [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_size_t)],
     "mm_cd_next_halo_planes": [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_size_t)],
     "mm_cd_update_planes": [_P, C.c_int, C.c_int],
+    "mm_cd_update_plane_ranges": [_P, C.POINTER(C.c_int), C.c_int],
     "mm_sim_config_default": [C.POINTER(mm_sim_config)],
     "mm_run": [C.POINTER(mm_sim_config), _fp, C.c_int, C.c_int, _fp, C.POINTER(mm_run_report)],
 }

@@ -225,6 +225,14 @@ struct mm_cd_engine {
         else
             fast->update(s, region, z_lo, z_hi, stream);
     }
+    void update_ranges(const int* r, int n) {
+        const StepParams s = params();
+        if (mode == MM_MODE_STRICT || !fast) {
+            for (int i = 0; i < n; ++i) strict_update(s, 0, r[2 * i], r[2 * i + 1], stream);
+        } else {
+            fast->update_ranges(s, r, n, stream);
+        }
+    }
     void finish_step(float amp, const int* src, const float* amp_dev, const int* step_dev) {
         if (src) launch_inject(p[in].ptr, cv.ptr, src_off(src), amp, amp_dev, step_dev, stream);
         if (free_surface && goff[2] == 0) launch_free_surface(p[in].ptr, lay, stream);
@@ -538,6 +546,17 @@ int mm_cd_update_planes(mm_cd_engine* e, int z_lo, int z_hi) {
     use(e);
     if (z_lo < 0 || z_hi > e->lay.n[2] || z_lo > z_hi) raise(ST_INVAL, "plane range out of bounds");
     e->update(0, z_lo, z_hi);
+    MM_API_END
+}
+
+int mm_cd_update_plane_ranges(mm_cd_engine* e, const int* ranges, int n) {
+    MM_API_BEGIN
+    use(e);
+    if (n < 0 || (n > 0 && !ranges)) raise(ST_INVAL, "plane ranges");
+    for (int i = 0; i < n; ++i)
+        if (ranges[2 * i] < 0 || ranges[2 * i + 1] > e->lay.n[2] || ranges[2 * i] > ranges[2 * i + 1])
+            raise(ST_INVAL, "plane range out of bounds");
+    e->update_ranges(ranges, n);
     MM_API_END
 }
 

@@ -295,6 +295,22 @@ public:
         }
     }
 
+    // p_next on the union of several plane ranges (the z-slab schedule's edge
+    // planes) with one launch per kernel
+    void update_ranges(const StepParams& p, const int* ranges, int n, cudaStream_t s) override {
+        ZRanges zr;
+        for (int i = 0; i < n; ++i)
+            if (ranges[2 * i + 1] > ranges[2 * i]) zr.emplace_back(ranges[2 * i], ranges[2 * i + 1]);
+        if (zr.empty()) return;
+        const bool fc = fast_cpml(p);
+        if (!fc) {
+            for (const auto& r : zr) update(p, 0, r.first, r.second, s);
+            return;
+        }
+        launch_inner(p, zr, zmode_ != 0 ? kFull : kInnerOnly, s);
+        launch_boundary(p, zr, s);
+    }
+
     void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
               const int* step_dev, cudaStream_t s) override {
         const bool fc = fast_cpml(p);
@@ -371,8 +387,11 @@ private:
     // Z slabs only
     enum InnerMode { kInnerOnly = 0, kFull = 1, kZSlabs = 2 };
 
-    static long long wkey(int z_lo, int z_hi, int mode) {
-        return ((long long)z_lo << 32) ^ ((long long)z_hi << 2) ^ mode;
+    using ZRanges = std::vector<std::pair<int, int>>;  // [z_lo, z_hi) plane ranges
+    static std::vector<int> wkey(const ZRanges& zr, int mode) {
+        std::vector<int> k{mode};
+        for (const auto& r : zr) k.push_back(r.first), k.push_back(r.second);
+        return k;
     }
 
     void finish_work(Work& w, const std::vector<Item>& tiles, int ctas, double target) {
@@ -384,8 +403,8 @@ private:
         w.ctr.set(std::vector<int>{0, 0}, stream_setup_);
     }
 
-    Work& inner_work(const StepParams& p, int z_lo, int z_hi, int mode) {
-        const auto key = wkey(z_lo, z_hi, mode);
+    Work& inner_work(const StepParams& p, const ZRanges& ranges, int mode) {
+        const auto key = wkey(ranges, mode);
         auto it = inner_cache_.find(key);
         if (it != inner_cache_.end()) return it->second;
         Work& w = inner_cache_[key];
@@ -396,16 +415,18 @@ private:
         if (inner.hi[0] <= inner.lo[0] || inner.hi[1] <= inner.lo[1]) return w;
         // z ranges of this launch
         std::vector<std::pair<int, int>> zr;
-        auto add = [&](int a, int b) {
-            a = std::max(a, z_lo);
-            b = std::min(b, z_hi);
-            if (b > a) zr.emplace_back(a, b);
-        };
-        if (mode == kInnerOnly) add(inner.lo[2], inner.hi[2]);
-        if (mode == kFull) add(0, lay_.n[2]);
-        if (mode == kZSlabs) {
-            add(0, inner.lo[2]);
-            add(inner.hi[2], lay_.n[2]);
+        for (const auto& rg : ranges) {
+            auto add = [&](int a, int b) {
+                a = std::max(a, rg.first);
+                b = std::min(b, rg.second);
+                if (b > a) zr.emplace_back(a, b);
+            };
+            if (mode == kInnerOnly) add(inner.lo[2], inner.hi[2]);
+            if (mode == kFull) add(0, lay_.n[2]);
+            if (mode == kZSlabs) {
+                add(0, inner.lo[2]);
+                add(inner.hi[2], lay_.n[2]);
+            }
         }
         if (zr.empty()) return w;
         w.empty = false;
@@ -421,8 +442,8 @@ private:
     }
 
     // X and Y slabs (the Z slabs go with the inner kernel)
-    Work& bnd_work(const StepParams& p, int z_lo, int z_hi) {
-        const auto key = wkey(z_lo, z_hi, 0);
+    Work& bnd_work(const StepParams& p, const ZRanges& ranges) {
+        const auto key = wkey(ranges, 0);
         auto it = bnd_cache_.find(key);
         if (it != bnd_cache_.end()) return it->second;
         Work& w = bnd_cache_[key];
@@ -439,8 +460,12 @@ private:
         for (const auto& s : slabs) {
             if ((s.first / 2 == 2 && zmode_ != 0) || !((kinds >> (s.first / 2)) & 1)) continue;
             const Box& b = s.second;
-            const int zl = std::max(b.lo[2], z_lo), zh = std::min(b.hi[2], z_hi);
-            if (zh <= zl) continue;
+            ZRanges zs;  // the box's planes within the launch's ranges
+            for (const auto& rg : ranges) {
+                const int zl = std::max(b.lo[2], rg.first), zh = std::min(b.hi[2], rg.second);
+                if (zh > zl) zs.emplace_back(zl, zh);
+            }
+            if (zs.empty()) continue;
             BndBox& bb = w.bboxes[w.nbox];
             for (int a = 0; a < 3; ++a) {
                 bb.lo[a] = b.lo[a];
@@ -451,9 +476,10 @@ private:
             bb.x_base = b.lo[0] & ~3;
             const int tiles_x = (b.hi[0] - bb.x_base + BC::TX - 1) / BC::TX;
             const int tiles_y = (b.hi[1] - b.lo[1] + BC::TY - 1) / BC::TY;
-            for (int ty = 0; ty < tiles_y; ++ty)
-                for (int tx = 0; tx < tiles_x; ++tx)
-                    items.push_back(Item{w.nbox | (tx << 3), ty, zl, zh});
+            for (const auto& z : zs)
+                for (int ty = 0; ty < tiles_y; ++ty)
+                    for (int tx = 0; tx < tiles_x; ++tx)
+                        items.push_back(Item{w.nbox | (tx << 3), ty, z.first, z.second});
             ++w.nbox;
         }
         if (items.empty()) return w;
@@ -463,12 +489,15 @@ private:
     }
 
     void launch_inner(const StepParams& p, int z_lo, int z_hi, int mode, cudaStream_t s) {
+        launch_inner(p, ZRanges{{z_lo, z_hi}}, mode, s);
+    }
+    void launch_inner(const StepParams& p, const ZRanges& zr, int mode, cudaStream_t s) {
         if (mode == kFull && zmode_ == 1) {  // inner box and Z slabs separately
-            launch_inner(p, z_lo, z_hi, kInnerOnly, s);
-            launch_inner(p, z_lo, z_hi, kZSlabs, s);
+            launch_inner(p, zr, kInnerOnly, s);
+            launch_inner(p, zr, kZSlabs, s);
             return;
         }
-        Work& w = inner_work(p, z_lo, z_hi, mode);
+        Work& w = inner_work(p, zr, mode);
         if (w.empty) return;
         InnerParams ip;
         std::memset(&ip, 0, sizeof ip);
@@ -578,8 +607,11 @@ private:
     }
 
     void launch_boundary(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) {
+        launch_boundary(p, ZRanges{{z_lo, z_hi}}, s);
+    }
+    void launch_boundary(const StepParams& p, const ZRanges& zr, cudaStream_t s) {
         if constexpr (kBnd && kP1) {
-            Work& w = bnd_work(p, z_lo, z_hi);
+            Work& w = bnd_work(p, zr);
             if (w.empty) return;
             refresh_run_maps(p);
             maps_.pc = bd_halo_[buf_index(p.pc)];
@@ -772,7 +804,7 @@ private:
     CpmlRun runs_[3][2] = {};
     bool runs_valid_ = false;
     cudaStream_t stream_setup_ = nullptr;
-    std::map<long long, Work> inner_cache_, bnd_cache_;
+    std::map<std::vector<int>, Work> inner_cache_, bnd_cache_;
     std::map<std::pair<int, int>, Pass1Work> pass1_cache_;
 };
 

@@ -14,6 +14,8 @@ public:
     virtual void pass1(const StepParams& p, cudaStream_t s) = 0;
     // Pass 2 + inner update on local planes [z_lo, z_hi); region as strict_update.
     virtual void update(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t s) = 0;
+    // Pass 2 + inner update on the union of n plane ranges [r[2i], r[2i+1]).
+    virtual void update_ranges(const StepParams& p, const int* ranges, int n, cudaStream_t s) = 0;
     // One whole step (pass 1, update, source injection); src_off < 0: no source.
     virtual void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
                       const int* step_dev, cudaStream_t s) = 0;

@@ -255,8 +255,9 @@ class ZSlabRank:
         """CPML pass 1 on every plane, then p_next on the r planes next to each
         cut (+ the source if it sits there, so neighbours receive it)."""
         self.e.update_boundary_psi()
-        for a, b in self._edges():
-            self.e.update_planes(a, b)
+        edges = self._edges()
+        if edges:  # both cuts' edge planes in one launch per kernel
+            self.e.update_plane_ranges(edges)
         if self._src_in_edges():
             self.e.inject_source(amp, self.src_local)
 

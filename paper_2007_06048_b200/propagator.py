@@ -180,6 +180,13 @@ class AcousticCdEngine:
     def update_planes(self, z_lo: int, z_hi: int):
         check(lib().mm_cd_update_planes(self._h, int(z_lo), int(z_hi)))
 
+    def update_plane_ranges(self, ranges):
+        """p_next on the union of plane ranges [(z_lo, z_hi), ...] in one launch per
+        kernel (the z-slab schedule's edge planes)."""
+        flat = [int(v) for r in ranges for v in r]
+        arr = (C.c_int * max(1, len(flat)))(*flat)
+        check(lib().mm_cd_update_plane_ranges(self._h, arr, len(flat) // 2))
+
     def inject_source(self, amp: float, src: Optional[Sequence[int]]):
         check(lib().mm_cd_inject_source(self._h, C.c_float(amp),
                                         _i3(*src) if src is not None else None))
