@@ -233,6 +233,65 @@ int mm_sim_config_default(mm_sim_config* cfg);
 int mm_run(const mm_sim_config* cfg, const float* vp_model, int device, int mode, float* traces,
            mm_run_report* report);
 
+/* ------------------------------------------------------------------------
+ * acoustic_iso: the variable-density first-order engine, SURVEY.md §8(f)
+ * row 4 (ref: AcousticVdEngine<float>, propagator.hpp:147-176, implemented at
+ * propagator_impl.hpp:175-295; driven by run(), driver.cpp:122-128).
+ * Same conventions as the acoustic_iso_cd engine above: host fields in the
+ * reference layout, every call asynchronous on the engine stream except the
+ * ones returning host data.  Arithmetic is the reference's association order
+ * (bit-identical results); there is one kernel family.
+ * --------------------------------------------------------------------- */
+typedef struct mm_vd_engine mm_vd_engine;
+
+/* ref: stencil.cpp:76-97 staggered_first_derivative_coeffs -> c[radius]. */
+int mm_staggered_first_derivative_coeffs(int radius, double h, double* c);
+/* ref: source.cpp:30-38 integrate_wavelet: out[s] = float(sum_{t<=s} w[t]*dt). */
+int mm_integrate_wavelet(const float* w, int n, double dt, float* out);
+
+/* ref: propagator_impl.hpp:175-212 ctor.  vp, rho: ghosted z-fastest model
+ * volumes (validated and ghost-replicated, as EarthModel holds them; copied).
+ * rho == NULL is the reference's "acoustic_iso requires a density volume"
+ * ValidationError.  vmax: the model's vmax (feeds the CPML profile). */
+int mm_vd_create(const mm_grid* grid, const float* vp, const float* rho,
+                 const mm_engine_options* opts, float dt, double vmax, int device,
+                 mm_vd_engine** out);
+int mm_vd_destroy(mm_vd_engine* e);
+/* ref: propagator.hpp:154-155 step(amp, src); amp is the time-integrated
+ * wavelet sample; src: 3 interior coordinates or NULL. */
+int mm_vd_step(mm_vd_engine* e, float amp, const int* src);
+/* Sub-phases of one step in the reference order (propagator_impl.hpp:275-295). */
+int mm_vd_update_velocity(mm_vd_engine* e);  /* update_velocity, :214-244 */
+int mm_vd_update_pressure(mm_vd_engine* e);  /* update_pressure, :246-273 */
+int mm_vd_inject_source(mm_vd_engine* e, float amp, const int* src); /* :287-291 */
+int mm_vd_apply_free_surface(mm_vd_engine* e);                       /* :292 */
+int mm_vd_synchronize(mm_vd_engine* e);
+int mm_vd_field_size(mm_vd_engine* e, size_t* count);
+int mm_vd_get_dt(mm_vd_engine* e, float* dt);
+int mm_vd_steps_taken(mm_vd_engine* e, long long* steps);
+/* ref: propagator.hpp:157-158 pressure() / velocity(axis): copies out
+ * (reference layout, ghosts included); set_* replace the device state (the
+ * reference hands out mutable references). */
+int mm_vd_get_pressure(mm_vd_engine* e, float* host);
+int mm_vd_get_velocity(mm_vd_engine* e, int axis, float* host);
+int mm_vd_set_pressure(mm_vd_engine* e, const float* host);
+int mm_vd_set_velocity(mm_vd_engine* e, int axis, const float* host);
+/* Receivers and the device-resident loop: as mm_cd_set_receivers /
+ * mm_cd_record / mm_cd_get_traces / mm_cd_copy_trace_step / mm_cd_run. */
+int mm_vd_set_receivers(mm_vd_engine* e, const int* ijk, int nreceivers, int capacity);
+int mm_vd_record(mm_vd_engine* e, int step);
+int mm_vd_get_traces(mm_vd_engine* e, float* host, int nsteps);
+int mm_vd_copy_trace_step(mm_vd_engine* e, int step, float* host, int async);
+int mm_vd_run(mm_vd_engine* e, const float* amps, int nsteps, const int* src, int record,
+              int first_sample, float* device_ms);
+int mm_vd_stream(mm_vd_engine* e, void** stream);
+/* ref: driver.cpp:83-144 run() with Propagator::AcousticIso: integrated
+ * Ricker source, default receiver carpet, per-step receiver-0 finiteness
+ * check.  vp_model, rho_model: ghosted z-fastest (validated / replicated
+ * here). */
+int mm_run_vd(const mm_sim_config* cfg, const float* vp_model, const float* rho_model,
+              int device, float* traces, mm_run_report* report);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

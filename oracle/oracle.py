@@ -174,6 +174,55 @@ class Oracle:
         return dict(traces=traces, dt=dt.value, kernel_seconds=ks.value,
                     modeling_seconds=ms.value)
 
+    # ---- acoustic_iso (variable density) --------------------------------
+    def staggered_first_derivative_coeffs(self, radius, h):
+        c = (C.c_double * 8)()
+        self._check(getattr(self.lib, self.p + "staggered_first_derivative_coeffs")(
+            C.c_int(radius), C.c_double(h), c))
+        return np.array(c[:radius])
+
+    def integrate_wavelet(self, w, dt):
+        w = np.ascontiguousarray(w, dtype=np.float32)
+        out = np.zeros_like(w)
+        fn = getattr(self.lib, self.p + "integrate_wavelet")
+        rc = fn(_f32(w), C.c_int(w.size), C.c_double(dt), _f32(out))
+        if self.kind != "port":
+            self._check(rc)
+        return out
+
+    def vd_engine(self, n, vp, rho, *, d=(20.0, 20.0, 20.0), radius=4, ndamping=(0, 0, 0),
+                  fmax=25.0, r_target=1e-3, free_surface=False, taper=False, ntaper=(3, 3, 3),
+                  dt=1e-3, vmax=None, nthreads=1):
+        return OracleVdEngine(self, n, vp, rho, d=d, radius=radius, ndamping=ndamping,
+                              fmax=fmax, r_target=r_target, free_surface=free_surface,
+                              taper=taper, ntaper=ntaper, dt=dt, vmax=vmax, nthreads=nthreads)
+
+    def run_vd(self, n, vp, rho, *, d=(20.0, 20.0, 20.0), radius=4, nsteps=100, fmax=25.0,
+               cfl=0.8, ndamping=(27, 27, 27), ntaper=(3, 3, 3), taper=True,
+               free_surface=False, r_target=1e-3, src=None, vmax=None, nthreads=1):
+        """minimod::run() for acoustic_iso (ref: driver.cpp:83-144, :122-128)."""
+        n = tuple(int(x) for x in n)
+        vp = np.ascontiguousarray(vp, dtype=np.float32)
+        rho = np.ascontiguousarray(rho, dtype=np.float32)
+        traces = np.zeros((n[0] * n[1], nsteps), np.float32)
+        dt, ks = C.c_double(), C.c_double()
+        srcp = _i3(*src) if src is not None else None
+        common = (_i3(*n), _d3(*d), C.c_int(radius), C.c_int(nsteps), C.c_double(fmax),
+                  C.c_double(cfl), _i3(*ndamping), _i3(*ntaper), C.c_int(int(taper)),
+                  C.c_int(int(free_surface)), C.c_double(r_target), srcp, _f32(vp), _f32(rho))
+        if self.kind == "port":
+            if vmax is None:
+                r = radius
+                vmax = float(vp[r:r + n[0], r:r + n[1], r:r + n[2]].max())
+            self._check(self.lib.mo_run_vd(*common, C.c_float(vmax), _f32(traces), C.byref(dt),
+                                           C.byref(ks)))
+            return dict(traces=traces, dt=dt.value, kernel_seconds=ks.value)
+        ms = C.c_double()
+        self._check(self.lib.ref_run_vd(*common, C.c_int(nthreads), _f32(traces), C.byref(dt),
+                                        C.byref(ks), C.byref(ms)))
+        return dict(traces=traces, dt=dt.value, kernel_seconds=ks.value,
+                    modeling_seconds=ms.value)
+
     # ---- on-disk formats and report (reference back end only) -----------
     def _ref_only(self):
         if self.kind != "reference":
@@ -296,6 +345,65 @@ class OracleEngine:
         rc = fn(self.h, _f32(a), _f32(b))
         if self.o.kind != "port":
             self.o._check(rc)
+
+
+class OracleVdEngine:
+    """AcousticVdEngine<float> (ref: propagator.hpp:147-176) on the CPU."""
+
+    def __init__(self, o: Oracle, n, vp, rho, *, d, radius, ndamping, fmax, r_target,
+                 free_surface, taper, ntaper, dt, vmax, nthreads):
+        self.o = o
+        self.n = tuple(int(x) for x in n)
+        self.r = radius
+        vp = np.ascontiguousarray(vp, dtype=np.float32)
+        rho = None if rho is None else np.ascontiguousarray(rho, dtype=np.float32)
+        self.shape = ghosted_shape(self.n, radius)
+        self.size = int(np.prod(self.shape))
+        h = C.c_void_p()
+        common = [_i3(*self.n), _d3(*d), C.c_int(radius), _f32(vp),
+                  _f32(rho) if rho is not None else None, _i3(*ndamping), C.c_double(fmax),
+                  C.c_double(r_target), C.c_int(int(free_surface)), C.c_int(int(taper)),
+                  _i3(*ntaper), C.c_float(dt)]
+        if o.kind == "port":
+            if vmax is None:
+                r = radius
+                vmax = float(vp[r:-r, r:-r, r:-r].max())
+            o._check(o.lib.mo_vd_create(*common, C.c_float(vmax), C.byref(h)))
+        else:
+            o._check(o.lib.ref_vd_create(*common, C.c_int(nthreads), C.byref(h)))
+        self.h = h
+        for name in ("vd_pressure",):
+            getattr(o.lib, o.p + name).restype = _fp
+        getattr(o.lib, o.p + "vd_velocity").restype = _fp
+        getattr(o.lib, o.p + "vd_destroy").argtypes = [C.c_void_p]
+        getattr(o.lib, o.p + "vd_step").argtypes = [C.c_void_p, C.c_float, C.c_void_p]
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            getattr(self.o.lib, self.o.p + "vd_destroy")(h)
+            self.h = None
+
+    def step(self, amp, src=None):
+        srcp = _i3(*src) if src is not None else None
+        self.o._check(getattr(self.o.lib, self.o.p + "vd_step")(self.h, C.c_float(amp), srcp))
+
+    def _view(self, ptr):
+        return np.ctypeslib.as_array(ptr, shape=(self.size,)).reshape(self.shape)
+
+    def pressure_view(self):
+        """Mutable view (the reference's pressure() returns a reference)."""
+        fn = getattr(self.o.lib, self.o.p + "vd_pressure")
+        fn.argtypes = [C.c_void_p]
+        return self._view(fn(self.h))
+
+    def pressure(self):
+        return self.pressure_view().copy()
+
+    def velocity(self, axis):
+        fn = getattr(self.o.lib, self.o.p + "vd_velocity")
+        fn.argtypes = [C.c_void_p, C.c_int]
+        return self._view(fn(self.h, axis)).copy()
 
 
 def nproc() -> int:

@@ -6,8 +6,8 @@
 // oracle/_ref/libminimod_ref.so.  It is used to pin the C restatement
 // (oracle/minimod_oracle.c) and as the "reference" CPU baseline in bench.py.
 // The shim only marshals arguments; every number comes from the reference's
-// AcousticCdEngine<float> (propagator_impl.hpp:53-173) and run()
-// (driver.cpp:83-144).
+// AcousticCdEngine<float> (propagator_impl.hpp:53-173), AcousticVdEngine<float>
+// (propagator_impl.hpp:175-295) and run() (driver.cpp:83-144).
 #include <cstring>
 #include <exception>
 #include <string>
@@ -318,6 +318,139 @@ int ref_render_report(const int ngrid[3], const double dgrid[3], int nsteps, dou
         const std::string s = render_parameter_block(c, m) + render_timing(rep);
         if ((int)s.size() + 1 > cap) throw std::invalid_argument("report buffer too small");
         std::memcpy(out, s.c_str(), s.size() + 1);
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+// ---------------------------------------------------------------- acoustic_iso
+// The variable-density engine AcousticVdEngine<float> (propagator_impl.hpp:
+// 175-295), its weights (stencil.cpp:76-97) and source (source.cpp:30-38), and
+// run() with Propagator::AcousticIso (driver.cpp:122-128).
+
+int ref_staggered_first_derivative_coeffs(int radius, double h, double* c) {
+    try {
+        const StencilCoeffs s = staggered_first_derivative_coeffs(radius, h);
+        for (int m = 0; m < radius; ++m) c[m] = s.c[m];
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+int ref_integrate_wavelet(const float* w, int n, double dt, float* out) {
+    try {
+        Wavelet in;
+        in.dt = dt;
+        in.samples.assign(w, w + n);
+        const Wavelet o = integrate_wavelet(in);
+        std::memcpy(out, o.samples.data(), sizeof(float) * n);
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+// vp, rho: ghosted z-fastest (validated + ghost-replicated by validate_model);
+// rho may be NULL (the engine then rejects the model).
+static EarthModel make_vd_model(const int n[3], const double d[3], int radius, const float* vp,
+                                const float* rho) {
+    EarthModel m;
+    m.grid = make_grid({n[0], n[1], n[2]}, {d[0], d[1], d[2]}, radius);
+    m.vp = Field(m.grid, "vp");
+    std::memcpy(m.vp.data.data(), vp, sizeof(float) * m.vp.data.size());
+    if (rho) {
+        m.rho = Field(m.grid, "rho");
+        std::memcpy(m.rho->data.data(), rho, sizeof(float) * m.rho->data.size());
+    }
+    validate_model(m);
+    return m;
+}
+
+struct ref_vd {
+    AcousticVdEngine<float>* eng;
+    int nthreads;
+};
+
+int ref_vd_create(const int n[3], const double d[3], int radius, const float* vp,
+                  const float* rho, const int ndamping[3], double fmax, double r_target,
+                  int free_surface, int taper, const int ntaper[3], float dt, int nthreads,
+                  ref_vd** out) {
+    try {
+        const EarthModel m = make_vd_model(n, d, radius, vp, rho);
+        EngineOptions o;
+        o.ndamping = {ndamping[0], ndamping[1], ndamping[2]};
+        o.fmax = fmax;
+        o.r_target = r_target;
+        o.free_surface = free_surface != 0;
+        o.taper = taper != 0;
+        o.ntaper = {ntaper[0], ntaper[1], ntaper[2]};
+        auto* e = new ref_vd;
+        e->eng = nullptr;
+        e->nthreads = nthreads < 1 ? 1 : nthreads;
+        try {
+            e->eng = new AcousticVdEngine<float>(m.grid, m, o, dt);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+void ref_vd_destroy(ref_vd* e) {
+    if (!e) return;
+    delete e->eng;
+    delete e;
+}
+
+int ref_vd_step(ref_vd* e, float amp, const int* src) {
+    try {
+        std::optional<std::array<int, 3>> s;
+        if (src) s = std::array<int, 3>{src[0], src[1], src[2]};
+        e->eng->step(amp, s, TaskRunner(e->nthreads));
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+float* ref_vd_pressure(ref_vd* e) { return e->eng->pressure().data.data(); }
+float* ref_vd_velocity(ref_vd* e, int axis) { return e->eng->velocity(axis).data.data(); }
+
+// run() with Propagator::AcousticIso (traces[r*nsteps+s]).
+int ref_run_vd(const int n[3], const double d[3], int radius, int nsteps, double fmax,
+               double cfl, const int ndamping[3], const int ntaper[3], int taper,
+               int free_surface, double r_target, const int* src_loc, const float* vp,
+               const float* rho, int nthreads, float* traces, double* dt_out,
+               double* kernel_seconds, double* modeling_seconds) {
+    try {
+        const EarthModel m = make_vd_model(n, d, radius, vp, rho);
+        SimConfig c;
+        c.propagator = Propagator::AcousticIso;
+        c.ngrid = {n[0], n[1], n[2]};
+        c.dgrid = {d[0], d[1], d[2]};
+        c.stencil_radius = radius;
+        c.nsteps = nsteps;
+        c.fmax = fmax;
+        c.cfl = cfl;
+        c.ndamping = {ndamping[0], ndamping[1], ndamping[2]};
+        c.ntaper = {ntaper[0], ntaper[1], ntaper[2]};
+        c.taper = taper != 0;
+        c.free_surface = free_surface != 0;
+        c.r_target = r_target;
+        if (src_loc) c.source_loc = std::array<int, 3>{src_loc[0], src_loc[1], src_loc[2]};
+        c.target = nthreads > 1 ? Target::Parallel : Target::Seq;
+        c.nthreads = nthreads > 1 ? nthreads : 1;
+        const auto [rec, rep] = run(c, m);
+        if (traces) std::memcpy(traces, rec.traces.data(), sizeof(float) * rec.traces.size());
+        if (dt_out) *dt_out = rep.dt;
+        if (kernel_seconds) *kernel_seconds = rep.kernel_seconds;
+        if (modeling_seconds) *modeling_seconds = rep.modeling_seconds;
         return 0;
     } catch (...) {
         return catch_all();

@@ -3,7 +3,8 @@
 Python front-end over the C-ABI CUDA library ``libminimod_b200.so``
 (include/minimod_b200.h).  Mirrors the reference's engine/driver interface:
 ``AcousticCdEngine``, ``EngineOptions``, ``SimConfig``, ``run``, ``cfl_dt``,
-``ricker``, ``default_layered_model`` ....
+``ricker``, ``default_layered_model`` ...; plus the next
+propagator, ``AcousticVdEngine`` (acoustic_iso, variable density).
 """
 from ._lib import (CollectiveError, ConfigError, CudaError, InstabilityError, MinimodError,
                    ValidationError, device_count, kernel_launch_count)
@@ -12,14 +13,15 @@ from .driver import (RunReport, SimConfig, build_geometry, cfl_dt, render_parame
 from .numerics import (AcquisitionGeometry, AxisCpml, CpmlProfile, EarthModel, Grid3D, IndexBox,
                        RegionPartition, ShotRecord, StencilCoeffs, Wavelet, build_profile,
                        central_first_derivative_coeffs, constant_model, default_layered_model,
-                       default_receivers, fill_ghosts_replicate, intersect, make_grid,
+                       default_receivers, fill_ghosts_replicate, integrate_wavelet, intersect,
+                       make_grid, staggered_first_derivative_coeffs,
                        partition_regions, random_model, ricker, second_derivative_coeffs,
                        taper_material, validate_model, version)
-from .propagator import AcousticCdEngine, EngineOptions
+from .propagator import AcousticCdEngine, AcousticVdEngine, EngineOptions
 from .shotio import load_model, load_record, save_model, save_record
 
 __all__ = [
-    "AcousticCdEngine", "EngineOptions", "SimConfig", "RunReport", "run", "cfl_dt",
+    "AcousticCdEngine", "AcousticVdEngine", "EngineOptions", "SimConfig", "RunReport", "run", "cfl_dt",
     "build_geometry", "Grid3D", "IndexBox", "RegionPartition", "make_grid", "partition_regions",
     "intersect", "fill_ghosts_replicate", "StencilCoeffs", "second_derivative_coeffs",
     "central_first_derivative_coeffs", "AxisCpml", "CpmlProfile", "build_profile",
@@ -28,5 +30,5 @@ __all__ = [
     "ShotRecord", "ConfigError", "ValidationError", "InstabilityError", "CudaError",
     "CollectiveError", "MinimodError", "device_count", "kernel_launch_count", "version",
     "render_parameter_block", "render_timing", "save_record", "load_record", "save_model",
-    "load_model",
+    "load_model", "staggered_first_derivative_coeffs", "integrate_wavelet",
 ]

@@ -133,6 +133,32 @@ SIGNATURES = {
     "mm_cd_update_plane_ranges": [_P, C.POINTER(C.c_int), C.c_int],
     "mm_sim_config_default": [C.POINTER(mm_sim_config)],
     "mm_run": [C.POINTER(mm_sim_config), _fp, C.c_int, C.c_int, _fp, C.POINTER(mm_run_report)],
+    # acoustic_iso (variable density)
+    "mm_staggered_first_derivative_coeffs": [C.c_int, C.c_double, _dp],
+    "mm_integrate_wavelet": [_fp, C.c_int, C.c_double, _fp],
+    "mm_vd_create": [C.POINTER(mm_grid), _fp, _fp, C.POINTER(mm_engine_options), C.c_float,
+                     C.c_double, C.c_int, C.POINTER(_P)],
+    "mm_vd_destroy": [_P],
+    "mm_vd_step": [_P, C.c_float, _ip],
+    "mm_vd_update_velocity": [_P],
+    "mm_vd_update_pressure": [_P],
+    "mm_vd_inject_source": [_P, C.c_float, _ip],
+    "mm_vd_apply_free_surface": [_P],
+    "mm_vd_synchronize": [_P],
+    "mm_vd_field_size": [_P, C.POINTER(C.c_size_t)],
+    "mm_vd_get_dt": [_P, _fp],
+    "mm_vd_steps_taken": [_P, C.POINTER(C.c_longlong)],
+    "mm_vd_get_pressure": [_P, _fp],
+    "mm_vd_get_velocity": [_P, C.c_int, _fp],
+    "mm_vd_set_pressure": [_P, _fp],
+    "mm_vd_set_velocity": [_P, C.c_int, _fp],
+    "mm_vd_set_receivers": [_P, _ip, C.c_int, C.c_int],
+    "mm_vd_record": [_P, C.c_int],
+    "mm_vd_get_traces": [_P, _fp, C.c_int],
+    "mm_vd_copy_trace_step": [_P, C.c_int, _fp, C.c_int],
+    "mm_vd_run": [_P, _fp, C.c_int, _ip, C.c_int, C.c_int, _fp],
+    "mm_vd_stream": [_P, C.POINTER(_P)],
+    "mm_run_vd": [C.POINTER(mm_sim_config), _fp, _fp, C.c_int, _fp, C.POINTER(mm_run_report)],
 }
 _RESTYPES = {
     "mm_last_error": C.c_char_p,
@@ -151,7 +177,7 @@ def lib() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python -m paper_2007_06048_b200.build` "
-            "(there is no CPU fallback for the acoustic_iso_cd engine)")
+            "(there is no CPU fallback for the engines)")
     L = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
     for name, args in SIGNATURES.items():
         fn = getattr(L, name)

@@ -30,6 +30,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
 EXTRA = {
     # strict kernels: reference operation order, never contract to FMA
     "kernels_strict.cu": ["-fmad=false"],
+    "vd_engine.cu": ["-fmad=false"],
     "kernels_fast.cu": ["-Xptxas", "-v"] if os.environ.get("MM_PTXAS_VERBOSE") else [],
 }
 

@@ -32,6 +32,13 @@ std::atomic<long long> g_launches{0};
 }  // namespace
 
 void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launches_so_far() { return g_launches.load(); }
+
+int set_api_error(int code, const std::string& msg, int step) {
+    g_err = msg;
+    g_step = step;
+    return code;
+}
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
     if (e != cudaSuccess)
@@ -51,35 +58,6 @@ Layout Layout::make(const int n[3], int r) {
     l.total = l.plane * l.ez;
     return l;
 }
-
-template <typename T>
-struct DevBuf {
-    T* ptr = nullptr;
-    size_t count = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() { reset(); }
-    void reset() {
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
-        count = 0;
-    }
-    void alloc(size_t n) {
-        reset();
-        if (n == 0) return;
-        MM_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
-        count = n;
-    }
-    void alloc_zero(size_t n, cudaStream_t s) {
-        alloc(n);
-        if (n) MM_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));
-    }
-    void upload(const T* host, size_t n, cudaStream_t s) {
-        if (count < n) alloc(n);
-        if (n) MM_CUDA(cudaMemcpyAsync(ptr, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
-    }
-};
 
 }  // namespace mmb
 
@@ -278,30 +256,6 @@ struct mm_cd_engine {
 };
 
 namespace {
-
-int set_error(int code, const std::string& msg, int step = 0) {
-    g_err = msg;
-    g_step = step;
-    return code;
-}
-
-#define MM_API_BEGIN try {
-#define MM_API_END                                                       \
-    }                                                                    \
-    catch (const mmb::Error& ex) {                                       \
-        return set_error(ex.code, ex.what(), ex.step);                   \
-    }                                                                    \
-    catch (const std::bad_alloc&) {                                      \
-        return set_error(MM_EINVAL, "host allocation failed");           \
-    }                                                                    \
-    catch (const std::exception& ex) {                                   \
-        return set_error(MM_EINVAL, ex.what());                          \
-    }                                                                    \
-    return MM_OK;
-
-void need(const void* p, const char* what) {
-    if (!p) raise(ST_INVAL, std::string(what) + " must not be NULL");
-}
 
 void use(mm_cd_engine* e) {
     need(e, "engine");

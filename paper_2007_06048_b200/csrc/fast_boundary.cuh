@@ -50,7 +50,10 @@ struct BndCfg {
     static constexpr int TILE_N = TX * TY, TILE = pad32(TILE_N);        // p_prev, c tiles
     // p_cur ring: the 2R+1-plane z window plus producer lead
     static constexpr int NS = MM_BND_NS > 2 * R + 1 ? MM_BND_NS : 2 * R + 2;
-    static constexpr int NQD = 8;  // stage barriers: at most NQD stages in flight
+#ifndef MM_BND_NQD
+#define MM_BND_NQD 8
+#endif
+    static constexpr int NQD = MM_BND_NQD;  // stage barriers: at most NQD stages in flight
     static constexpr int NBAR = 2 * NS + 2 * NQD + 4;
     // bytes per CTA: two CTAs per SM up to R = 4; one (with the registers of
     // two) for wider stencils, whose z window needs a deeper ring

@@ -4,6 +4,8 @@
 // precision per operation, same association order), which the parity tests
 // check against the reference build (tests/test_host_numerics.py):
 //   second_derivative / central_first_derivative  ref: stencil.cpp:9-31,50-74,99-117
+//   staggered_first_derivative                    ref: stencil.cpp:76-97
+//   integrate_wavelet                             ref: source.cpp:30-38
 //   cfl_dt                                        ref: driver.cpp:19-29
 //   ricker                                        ref: source.cpp:11-28
 //   build_profile                                 ref: cpml.hpp:34-72
@@ -27,9 +29,10 @@ void require_stencil(int radius, double h) {
 }
 
 // Taylor-matching system for symmetric (odd = false) or antisymmetric
-// (odd = true) collocated taps on unit spacing: row k demands that the taps
-// reproduce the 2k-th (resp. (2k-1)-th) derivative of x^q exactly.
-std::vector<double> taylor_solve(int radius, bool odd) {
+// (odd = true) taps on unit spacing: row k demands that the taps reproduce
+// the 2k-th (resp. (2k-1)-th) derivative of x^q exactly.  Nodes sit at x = m
+// (collocated) or x = m - 1/2 (staggered).
+std::vector<double> taylor_solve(int radius, bool odd, bool staggered = false) {
     const int n = radius;
     std::vector<long double> A(static_cast<size_t>(n) * n), rhs(n, 0.0L);
     rhs[0] = 1.0L;
@@ -38,7 +41,11 @@ std::vector<double> taylor_solve(int radius, bool odd) {
         long double qfact = 1;
         for (int f = 2; f <= q; ++f) qfact *= f;
         for (int m = 1; m <= n; ++m)
-            A[(k - 1) * n + (m - 1)] = 2.0L * powl(static_cast<long double>(m), q) / qfact;
+            A[(k - 1) * n + (m - 1)] =
+                2.0L * powl(staggered ? static_cast<long double>(m) - 0.5L
+                                      : static_cast<long double>(m),
+                            q) /
+                qfact;
     }
     // Forward elimination, partial pivoting on double-rounded magnitudes.
     for (int col = 0; col < n; ++col) {
@@ -86,6 +93,24 @@ Coeffs central_first_derivative(int radius, double h) {
     Coeffs out;
     out.c = taylor_solve(radius, true);
     for (double& v : out.c) v /= h;
+    return out;
+}
+
+Coeffs staggered_first_derivative(int radius, double h) {
+    require_stencil(radius, h);
+    Coeffs out;
+    out.c = taylor_solve(radius, true, true);
+    for (double& v : out.c) v /= h;
+    return out;
+}
+
+std::vector<float> integrate_wavelet(const std::vector<float>& w, double dt) {
+    std::vector<float> out(w.size());
+    double acc = 0.0;
+    for (size_t s = 0; s < w.size(); ++s) {
+        acc += static_cast<double>(w[s]) * dt;
+        out[s] = static_cast<float>(acc);
+    }
     return out;
 }
 

@@ -37,6 +37,27 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 
 // Counts kernel launches issued through the library (evidence for bench.py).
 void note_launches(long long n);
+long long launches_so_far();
+
+// C-ABI error plumbing (engine.cu): records the thread-local message/step
+// behind mm_last_error() and returns the status code.
+int set_api_error(int code, const std::string& msg, int step = 0);
+inline void need(const void* p, const char* what) {
+    if (!p) raise(ST_INVAL, std::string(what) + " must not be NULL");
+}
+#define MM_API_BEGIN try {
+#define MM_API_END                                                       \
+    }                                                                    \
+    catch (const ::mmb::Error& ex) {                                     \
+        return ::mmb::set_api_error(ex.code, ex.what(), ex.step);        \
+    }                                                                    \
+    catch (const std::bad_alloc&) {                                      \
+        return ::mmb::set_api_error(MM_EINVAL, "host allocation failed"); \
+    }                                                                    \
+    catch (const std::exception& ex) {                                   \
+        return ::mmb::set_api_error(MM_EINVAL, ex.what());               \
+    }                                                                    \
+    return MM_OK;
 
 // ---------------------------------------------------------------- numerics
 // All of these restate the reference bit for bit (see host_numerics.cpp).
@@ -46,6 +67,8 @@ struct Coeffs {
 };
 Coeffs second_derivative(int radius, double h);      // ref: stencil.cpp:50-74
 Coeffs central_first_derivative(int radius, double h);  // ref: stencil.cpp:99-117
+Coeffs staggered_first_derivative(int radius, double h);  // ref: stencil.cpp:76-97
+std::vector<float> integrate_wavelet(const std::vector<float>& w, double dt);  // source.cpp:30-38
 double cfl_dt(double vmax, const int n[3], const double d[3], int radius, double cfl);
 std::vector<float> ricker(double fmax, double dt, int nsteps);
 
@@ -72,6 +95,36 @@ void taper_material(float* f, const HostGrid& g, const int ntaper[3], const int 
 void validate_vp(const float* vp, const HostGrid& g, float* vmin, float* vmax);
 
 // ---------------------------------------------------------------- device
+// Owning device allocation (engine-lifetime buffers).
+template <typename T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        count = 0;
+    }
+    void alloc(size_t n) {
+        reset();
+        if (n == 0) return;
+        MM_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+        count = n;
+    }
+    void alloc_zero(size_t n, cudaStream_t s) {
+        alloc(n);
+        if (n) MM_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));
+    }
+    void upload(const T* host, size_t n, cudaStream_t s) {
+        if (count < n) alloc(n);
+        if (n) MM_CUDA(cudaMemcpyAsync(ptr, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
 struct Layout {
     int n[3];
     int r, L, P, ey, ez;

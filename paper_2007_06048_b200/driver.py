@@ -1,9 +1,12 @@
-"""run() -- the reference's modeling driver on the GPU (acoustic_iso_cd only).
+"""run() -- the reference's modeling driver on the GPU.
 
 ref: driver.hpp:21-54 (SimConfig, RunReport), driver.cpp:19-29 (cfl_dt),
-driver.cpp:37-47 (build_geometry), driver.cpp:83-144 (run).  The time loop
-itself runs in C++ (``mm_run`` in csrc/engine.cu): device-resident wavelet,
-device receiver recording, one receiver-0 finiteness check per step.
+driver.cpp:37-47 (build_geometry), driver.cpp:83-144 (run).  Two propagators:
+``acoustic_iso_cd`` (the hot path) and ``acoustic_iso`` (variable density,
+SURVEY.md §8(f) row 4; integrated Ricker source, driver.cpp:122-128).  The
+time loop itself runs in C++ (``mm_run`` in csrc/engine.cu, ``mm_run_vd`` in
+csrc/vd_engine.cu): device-resident wavelet, device receiver recording, one
+receiver-0 finiteness check per step.
 ``kernel_seconds`` is the device time of the step loop (CUDA events), the
 analogue of the reference's "Time Kernel" (driver.cpp:102-107).
 """
@@ -16,13 +19,14 @@ from typing import Optional, Tuple
 import numpy as np
 
 from . import _lib
-from ._lib import ConfigError, check, lib
+from ._lib import ConfigError, ValidationError, check, lib
 from .numerics import (AcquisitionGeometry, EarthModel, Grid3D, ShotRecord, default_receivers,
                        make_grid)
 
 
 @dataclass
-class SimConfig:  # ref: driver.hpp:21-47 (acoustic_iso_cd subset, same defaults)
+class SimConfig:  # ref: driver.hpp:21-47 (same defaults; no elastic_iso)
+    propagator: str = "acoustic_iso_cd"
     ngrid: tuple = (100, 100, 100)
     dgrid: tuple = (20.0, 20.0, 20.0)
     nsteps: int = 1000
@@ -86,9 +90,18 @@ def build_geometry(config: SimConfig, grid: Grid3D) -> AcquisitionGeometry:
     return g
 
 
+PROPAGATORS = ("acoustic_iso_cd", "acoustic_iso")
+
+
 def run(config: SimConfig, model: EarthModel, *, device: int = 0,
         mode: str = "fast") -> Tuple[ShotRecord, RunReport]:
-    """ref: driver.cpp:83-144 for acoustic_iso_cd."""
+    """ref: driver.cpp:83-144.  ``mode`` selects the acoustic_iso_cd kernel
+    family (acoustic_iso has one)."""
+    if config.propagator not in PROPAGATORS:
+        raise ConfigError(f"unknown propagator '{config.propagator}' (this build: "
+                          f"{', '.join(PROPAGATORS)})")
+    if config.nsteps < 1:
+        raise ConfigError("nsteps must be >= 1")
     if tuple(model.grid.n) != tuple(config.ngrid):
         raise ConfigError("model grid does not match configured ngrid")
     grid = make_grid(config.ngrid, config.dgrid, config.stencil_radius)
@@ -98,6 +111,15 @@ def run(config: SimConfig, model: EarthModel, *, device: int = 0,
         raise ConfigError("model radius does not match the stencil radius")
     traces = np.zeros((geom.nreceivers(), config.nsteps), np.float32)
     rep = _lib.mm_run_report()
+    if config.propagator == "acoustic_iso":
+        if model.rho is None:
+            raise ValidationError("acoustic_iso requires a density volume (rho)")
+        rho = np.ascontiguousarray(model.rho, dtype=np.float32)
+        check(lib().mm_run_vd(C.byref(config.to_c()), vp.ctypes.data_as(C.POINTER(C.c_float)),
+                              rho.ctypes.data_as(C.POINTER(C.c_float)), int(device),
+                              traces.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rep)))
+        record = ShotRecord(config.nsteps, rep.dt, geom, traces)
+        return record, RunReport(rep.dt, rep.kernel_seconds, rep.modeling_seconds, rep.steps_run)
     from .propagator import _MODES
     check(lib().mm_run(C.byref(config.to_c()), vp.ctypes.data_as(C.POINTER(C.c_float)),
                        int(device), _MODES[mode],

@@ -4,12 +4,14 @@ Python mirror of the reference's setup layer; every number is computed by the
 C++ library (``csrc/host_numerics.cpp``), bit-identical to the reference:
 
 * ``Grid3D`` / ``make_grid`` / ``partition_regions``  -- ref: grid.hpp, grid.cpp
-* ``second_derivative_coeffs`` / ``central_first_derivative_coeffs`` -- ref: stencil.cpp
+* ``second_derivative_coeffs`` / ``central_first_derivative_coeffs`` /
+  ``staggered_first_derivative_coeffs``               -- ref: stencil.cpp
 * ``build_profile``                                    -- ref: cpml.hpp:34-72
 * ``taper_material`` / ``fill_ghosts_replicate``       -- ref: propagator.hpp:36-62, grid.hpp:96-108
 * ``EarthModel`` / ``default_layered_model`` / ``constant_model`` / ``validate_model``
                                                        -- ref: model.hpp, model.cpp
-* ``ricker`` / ``default_receivers`` / ``ShotRecord``   -- ref: source.hpp, source.cpp
+* ``ricker`` / ``integrate_wavelet`` / ``default_receivers`` / ``ShotRecord``
+                                                       -- ref: source.hpp, source.cpp
 
 Fields are numpy float32 arrays in the reference layout: ghosted, z fastest,
 shape ``(nx+2r, ny+2r, nz+2r)`` (ref: grid.hpp:61-65).
@@ -172,6 +174,13 @@ def central_first_derivative_coeffs(radius: int, h: float) -> StencilCoeffs:
     return StencilCoeffs(radius, h, np.array(c[:radius]), 0.0)
 
 
+def staggered_first_derivative_coeffs(radius: int, h: float) -> StencilCoeffs:
+    """ref: stencil.cpp:76-97 (acoustic_iso's half-cell derivative)."""
+    c = (C.c_double * 8)()
+    check(lib().mm_staggered_first_derivative_coeffs(radius, h, c))
+    return StencilCoeffs(radius, h, np.array(c[:radius]), 0.0)
+
+
 # ---------------------------------------------------------------------- CPML
 @dataclass
 class AxisCpml:  # ref: cpml.hpp:13-18
@@ -215,11 +224,15 @@ def taper_material(f: np.ndarray, ntaper, offset, global_n, grid: Grid3D) -> np.
 
 # --------------------------------------------------------------------- model
 @dataclass
-class EarthModel:  # ref: model.hpp:13-25 (vp only: acoustic_iso_cd needs no rho/vs)
+class EarthModel:  # ref: model.hpp:13-25 (vp, optional rho; vs is elastic-only)
     grid: Grid3D
     vp: np.ndarray
     vmin: float = 0.0
     vmax: float = 0.0
+    rho: Optional[np.ndarray] = None  # acoustic_iso only
+
+    def has_rho(self) -> bool:
+        return self.rho is not None
 
 
 def validate_model(m: EarthModel) -> EarthModel:  # ref: model.cpp:15-43
@@ -228,11 +241,19 @@ def validate_model(m: EarthModel) -> EarthModel:  # ref: model.cpp:15-43
     check(lib().mm_validate_model(_i3(*m.grid.n), m.grid.radius, _fptr(m.vp), C.byref(vmin),
                                   C.byref(vmax)))
     m.vmin, m.vmax = vmin.value, vmax.value
+    if m.rho is not None:
+        m.rho = np.ascontiguousarray(m.rho, dtype=np.float32)
+        inner = m.grid.inner(m.rho)
+        if not (np.isfinite(inner).all() and (inner > 0.0).all()):
+            raise ValidationError("rho must be finite and > 0 everywhere")
+        fill_ghosts_replicate(m.rho, m.grid)
     return m
 
 
-def constant_model(grid: Grid3D, vp: float) -> EarthModel:  # ref: model.cpp:45-61
-    return validate_model(EarthModel(grid, grid.field(vp)))
+def constant_model(grid: Grid3D, vp: float, rho: Optional[float] = None) -> EarthModel:
+    """ref: model.cpp:45-61 (vs omitted: elastic only)."""
+    return validate_model(EarthModel(grid, grid.field(vp), rho=None if rho is None
+                                     else grid.field(rho)))
 
 
 def default_layered_model(grid: Grid3D) -> EarthModel:  # ref: model.cpp:63-77
@@ -240,7 +261,7 @@ def default_layered_model(grid: Grid3D) -> EarthModel:  # ref: model.cpp:63-77
     vmin, vmax = C.c_float(), C.c_float()
     check(lib().mm_layered_model(_i3(*grid.n), grid.radius, _fptr(vp), C.byref(vmin),
                                  C.byref(vmax)))
-    return EarthModel(grid, vp, vmin.value, vmax.value)
+    return EarthModel(grid, vp, vmin.value, vmax.value, rho=grid.field(1000.0))
 
 
 def random_model(grid: Grid3D, lo: float = 1500.0, hi: float = 4500.0,
@@ -266,6 +287,16 @@ def ricker(fmax: float, dt: float, nsteps: int) -> Wavelet:  # ref: source.cpp:1
     out = np.zeros(max(nsteps, 0), np.float32)
     check(lib().mm_ricker(fmax, dt, nsteps, _fptr(out) if nsteps > 0 else None))
     return Wavelet(out, dt, fmax, 1.5 / (fmax / 2.5))
+
+
+def integrate_wavelet(w: Wavelet) -> Wavelet:  # ref: source.cpp:30-38
+    """Running time integral (double accumulator): the source of the
+    first-order acoustic_iso system."""
+    src = np.ascontiguousarray(w.samples, dtype=np.float32)
+    out = np.zeros_like(src)
+    if src.size:
+        check(lib().mm_integrate_wavelet(_fptr(src), src.size, float(w.dt), _fptr(out)))
+    return Wavelet(out, w.dt, w.fmax, w.t0)
 
 
 @dataclass

@@ -249,3 +249,152 @@ class AcousticCdEngine:
         fn = lib().mm_cd_next_halo_planes if next_field else lib().mm_cd_halo_planes
         check(fn(self._h, int(side), int(which), C.byref(p), C.byref(n)))
         return p.value, n.value
+
+
+class AcousticVdEngine:
+    """Variable-density first-order acoustic propagator with CPML on the GPU.
+
+    ref: propagator.hpp:147-176 (interface), propagator_impl.hpp:175-295;
+    SURVEY.md §8(f) row 4.  ``model`` must carry a density volume (rho), as
+    the reference requires (propagator_impl.hpp:186-187).  ``step`` takes the
+    time-integrated wavelet sample (numerics.integrate_wavelet).
+    """
+
+    def __init__(self, grid: Grid3D, model, opts: Optional[EngineOptions] = None,
+                 dt: float = 1e-3, *, device: int = 0):
+        opts = opts or EngineOptions()
+        self._h = None
+        self._grid = grid
+        vp = np.ascontiguousarray(model.vp, dtype=np.float32)
+        rho = None if model.rho is None else np.ascontiguousarray(model.rho, dtype=np.float32)
+        if vp.shape != grid.shape or (rho is not None and rho.shape != grid.shape):
+            raise ValueError("model volumes must have the ghosted grid shape")
+        vmax = model.vmax if model.vmax else float(grid.inner(vp).max())
+        g = _lib.mm_grid()
+        g.n[:] = list(grid.n)
+        g.d[:] = list(grid.d)
+        g.radius = grid.radius
+        h = C.c_void_p()
+        check(lib().mm_vd_create(C.byref(g), _fptr(vp), _fptr(rho) if rho is not None else None,
+                                 C.byref(opts.to_c()), C.c_float(dt), float(vmax), int(device),
+                                 C.byref(h)))
+        self._h = h
+        self.device = device
+        self.options = opts
+        self._nrec = 0
+        self._cap = 0
+
+    def close(self):
+        if self._h:
+            lib().mm_vd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- reference interface ---------------------------------------------
+    def step(self, source_amplitude: float, src: Optional[Sequence[int]] = None, runner=None):
+        """ref: propagator.hpp:154-155."""
+        check(lib().mm_vd_step(self._h, C.c_float(source_amplitude),
+                               _i3(*src) if src is not None else None))
+
+    def grid(self) -> Grid3D:
+        return self._grid
+
+    def dt(self) -> float:
+        v = C.c_float()
+        check(lib().mm_vd_get_dt(self._h, C.byref(v)))
+        return v.value
+
+    def pressure(self) -> np.ndarray:
+        """ref: propagator.hpp:157 (a copy; see set_pressure)."""
+        out = self._grid.field()
+        check(lib().mm_vd_get_pressure(self._h, _fptr(out)))
+        return out
+
+    def velocity(self, axis: int) -> np.ndarray:
+        """ref: propagator.hpp:158 (a copy; see set_velocity)."""
+        out = self._grid.field()
+        check(lib().mm_vd_get_velocity(self._h, int(axis), _fptr(out)))
+        return out
+
+    def set_pressure(self, p: np.ndarray):
+        a = np.ascontiguousarray(p, dtype=np.float32)
+        if a.shape != self._grid.shape:
+            raise ValueError("pressure must have the ghosted grid shape")
+        check(lib().mm_vd_set_pressure(self._h, _fptr(a)))
+
+    def set_velocity(self, axis: int, v: np.ndarray):
+        a = np.ascontiguousarray(v, dtype=np.float32)
+        if a.shape != self._grid.shape:
+            raise ValueError("velocity must have the ghosted grid shape")
+        check(lib().mm_vd_set_velocity(self._h, int(axis), _fptr(a)))
+
+    # -- sub-phases (ref: propagator_impl.hpp:275-295) --------------------
+    def update_velocity(self):
+        check(lib().mm_vd_update_velocity(self._h))
+
+    def update_pressure(self):
+        check(lib().mm_vd_update_pressure(self._h))
+
+    def inject_source(self, amp: float, src: Sequence[int]):
+        check(lib().mm_vd_inject_source(self._h, C.c_float(amp), _i3(*src)))
+
+    def apply_free_surface(self):
+        check(lib().mm_vd_apply_free_surface(self._h))
+
+    def synchronize(self):
+        check(lib().mm_vd_synchronize(self._h))
+
+    def steps_taken(self) -> int:
+        v = C.c_longlong()
+        check(lib().mm_vd_steps_taken(self._h, C.byref(v)))
+        return v.value
+
+    # -- receivers / device loop -----------------------------------------
+    def set_receivers(self, ijk: np.ndarray, capacity: int):
+        ijk = np.ascontiguousarray(ijk, dtype=np.int32).reshape(-1, 3)
+        check(lib().mm_vd_set_receivers(self._h, ijk.ctypes.data_as(C.POINTER(C.c_int)),
+                                        ijk.shape[0], int(capacity)))
+        self._nrec, self._cap = ijk.shape[0], int(capacity)
+
+    def record(self, step: int):
+        check(lib().mm_vd_record(self._h, int(step)))
+
+    def traces(self, nsteps: Optional[int] = None) -> np.ndarray:
+        nsteps = self._cap if nsteps is None else nsteps
+        out = np.zeros((self._nrec, nsteps), np.float32)
+        check(lib().mm_vd_get_traces(self._h, _fptr(out), int(nsteps)))
+        return out
+
+    def copy_trace_step(self, step: int, out: np.ndarray, asynchronous: bool = False):
+        assert out.dtype == np.float32 and out.size >= self._nrec
+        check(lib().mm_vd_copy_trace_step(self._h, int(step), _fptr(out), int(asynchronous)))
+
+    def run(self, amps: np.ndarray, src: Optional[Sequence[int]] = None, record: bool = True,
+            first_sample: int = 0) -> float:
+        """Device-resident loop over len(amps) steps; returns device milliseconds."""
+        amps = np.ascontiguousarray(amps, dtype=np.float32)
+        ms = C.c_float()
+        check(lib().mm_vd_run(self._h, _fptr(amps), amps.size,
+                              _i3(*src) if src is not None else None, int(record),
+                              int(first_sample), C.byref(ms)))
+        return ms.value
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        check(lib().mm_vd_stream(self._h, C.byref(s)))
+        return s.value or 0

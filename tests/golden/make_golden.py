@@ -3,10 +3,10 @@
 Run in the authoring container, where /root/reference exists and
 `make -C oracle` has built oracle/_ref/libminimod_ref.so:
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [all|cd|vd]
 
-Every array below comes from the reference's own AcousticCdEngine<float> /
-run() (through oracle/ref_shim.cpp); nothing is computed by this repo's code.
+Every array below comes from the reference's own AcousticCdEngine<float>,
+AcousticVdEngine<float> and run() (through oracle/ref_shim.cpp); nothing is computed by this repo's code.
 Inputs (vp models) are stored alongside, so the fixtures are self-contained.
 """
 import sys
@@ -106,9 +106,54 @@ def checksum_case():
     print("run_layered_100 dt", out["dt"])
 
 
+# acoustic_iso (variable density): AcousticVdEngine<float>
+VD_CASES = {
+    # name: (n, r, ndamping, free_surface, taper, steps, dt, seed)
+    "vd_cpml": ((22, 26, 30), 4, (5, 6, 7), False, True, 40, 1.0e-3, 41),
+    "vd_r2_fs": ((24, 20, 28), 2, (6, 4, 5), True, False, 40, 1.0e-3, 42),
+    "vd_r8": ((34, 34, 36), 8, (5, 6, 7), False, False, 25, 1.0e-3, 43),
+}
+
+
+def vd_case(name, n, r, nd, fs, taper, steps, dt, seed):
+    vp = rand_vp(n, r, seed)
+    rho = rand_vp(n, r, seed + 100, 1000.0, 2500.0)
+    e = R.vd_engine(n, vp, rho, radius=r, ndamping=nd, free_surface=fs, taper=taper, dt=dt)
+    w = R.integrate_wavelet(R.ricker(25.0, dt, steps), dt)
+    src = tuple(x // 2 for x in n)
+    rec = []
+    for s in range(steps):
+        e.step(w[s], src)
+        rec.append(e.pressure()[r:-r, r:-r, r + nd[2]].copy())
+    np.savez_compressed(
+        OUT / f"{name}.npz", n=np.array(n), radius=r, ndamping=np.array(nd), free_surface=int(fs),
+        taper=int(taper), steps=steps, dt=np.float32(dt), src=np.array(src), vp=vp, rho=rho,
+        wavelet=w, p=e.pressure(), vx=e.velocity(0), vy=e.velocity(1), vz=e.velocity(2),
+        surface=np.stack(rec).astype(np.float32))
+    print(name, "max|p|", float(np.abs(e.pressure()).max()))
+
+
+def vd_run_case():
+    """driver run() with Propagator::AcousticIso: 32^3 layered (rho 1000)."""
+    n = (32, 32, 32)
+    vp, vmin, vmax = R.layered_model(n)
+    rho = np.full_like(vp, 1000.0)
+    out = R.run_vd(n, vp, rho, nsteps=60, ndamping=(4, 4, 4), ntaper=(2, 2, 2))
+    np.savez_compressed(OUT / "run_vd_layered_32.npz", n=np.array(n), nsteps=60,
+                        ndamping=np.array((4, 4, 4)), ntaper=np.array((2, 2, 2)),
+                        traces=out["traces"], dt=out["dt"])
+    print("run_vd_layered_32 dt", out["dt"], "max", float(np.abs(out["traces"]).max()))
+
+
 if __name__ == "__main__":
-    for name, args in ENGINE_CASES.items():
-        engine_case(name, *args)
-    degenerate_case()
-    run_case()
-    checksum_case()
+    only = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if only in ("all", "cd"):
+        for name, args in ENGINE_CASES.items():
+            engine_case(name, *args)
+        degenerate_case()
+        run_case()
+        checksum_case()
+    if only in ("all", "vd"):
+        for name, args in VD_CASES.items():
+            vd_case(name, *args)
+        vd_run_case()
