@@ -86,6 +86,14 @@ CUtensorMap run_map(const Layout& L, const CpmlRun& r, int ax, const float* base
     return make_map(base, r.s1, L.n[1], w, r.s1, r.s2, bx, by);
 }
 
+}  // namespace
+
+CUtensorMap tma_field_map(const Layout& L, const float* base, int bx, int by) {
+    return field_map(L, base, bx, by);
+}
+
+namespace {
+
 template <typename T>
 struct DArr {
     T* ptr = nullptr;

@@ -1,11 +1,17 @@
 // mm_fast.hpp -- the MM_MODE_FAST step (TMA-fed 2.5D kernels), see kernels_fast.cu.
 #pragma once
 
+#include <cuda.h>
+
 #include <memory>
 
 #include "mm_internal.hpp"
 
 namespace mmb {
+
+// 3D fp32 TMA tensor map (x fastest, box bx x by x 1, out-of-bounds reads
+// zero) over a device-layout field; shared with the acoustic_iso engine.
+CUtensorMap tma_field_map(const Layout& L, const float* base, int bx, int by);
 
 class FastPlan {
 public:

@@ -11,12 +11,13 @@
 //   psi = b psi + a d;  d = d ik + psi.
 //
 // Device layout: the engine-wide one (mm_internal.hpp, x fastest, z slowest).
-// Two kernels per step, each a z-streaming sweep: a thread owns one (x, y)
-// column over a z chunk and keeps the 2R-point z window of the differentiated
-// field in registers; x and y neighbours come through L1.  Bytes per point
-// and step (compulsory): velocity p, dt/rho, v (r+w) = 32 B; pressure v, dtb,
-// p (r+w) = 24 B -- 56 B against the reference cost model's fused 40 B
-// (bench.cpp:97), see DESIGN.md.
+// Two kernels per step (vd_fast.cuh): k_vdv (velocity) and k_vdp (pressure),
+// TMA-fed 2.5D sweeps along z.  Bytes per point and step (compulsory):
+// velocity p, dt/rho, v (r+w) = 32 B; pressure v, dtb, p (r+w) = 24 B --
+// 56 B against the reference cost model's fused 40 B (bench.cpp:97), see
+// DESIGN.md.  The one-thread-per-point kernels below (k_vd_velocity /
+// k_vd_pressure) are the plain restatement, kept for A/B checks
+// (MM_VD_SIMPLE=1); both families are bit-identical.
 //
 // CPML memory lives only where it can be non-zero: one array per axis, per
 // damping layer along that axis and per pass (the "runs" of mm_internal.hpp).
@@ -38,7 +39,9 @@
 #include <vector>
 
 #include "../../include/minimod_b200.h"
+#include "mm_fast.hpp"
 #include "mm_internal.hpp"
+#include "vd_fast.cuh"
 
 namespace mmb {
 namespace vd {
@@ -204,6 +207,98 @@ void launch(bool velocity, const VdParams& P, cudaStream_t s) {
     }
 }
 
+// TMA plan: tensor maps, work items and queues of k_vdv / k_vdp.
+template <int R>
+struct FastVd {
+    using C = vdk::VdCfg<R>;
+    CUtensorMap tm_p, tm_vx, tm_vy, tm_vz;
+    DevBuf<int4> items;
+    DevBuf<int> ctr;  // [0..1] velocity queue, [2..3] pressure queue
+    int nitems = 0, grid_v = 0, grid_p = 0;
+
+    FastVd(const Layout& L, float* p, float* const v[3], int device, cudaStream_t s) {
+        tm_p = tma_field_map(L, p, C::BX, C::BY);
+        tm_vx = tma_field_map(L, v[0], C::BX, C::TY);
+        tm_vy = tma_field_map(L, v[1], C::TX, C::BY);
+        tm_vz = tma_field_map(L, v[2], C::TX, C::TY);
+        MM_CUDA(cudaFuncSetAttribute(vdk::k_vdv<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)C::SMEM_V));
+        MM_CUDA(cudaFuncSetAttribute(vdk::k_vdp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)C::SMEM_P));
+        int sms = 0, ov = 0, op = 0;
+        MM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ov, vdk::k_vdv<R>, C::NT, C::SMEM_V));
+        MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&op, vdk::k_vdp<R>, C::NT, C::SMEM_P));
+        if (ov < 1 || op < 1) raise(ST_CUDA, "acoustic_iso kernels do not fit on an SM");
+        // (tile, z-chunk) items, chunk-major; about 4 items per resident CTA
+        const int tx = (L.n[0] + C::TX - 1) / C::TX, ty = (L.n[1] + C::TY - 1) / C::TY;
+        const int slots = sms * std::max(ov, op);
+        int nch = std::max(1, (4 * slots + tx * ty - 1) / (tx * ty));
+        nch = std::min(nch, std::max(1, L.n[2] / 8));
+        if (const char* e = std::getenv("MM_VD_ZCHUNKS")) nch = std::max(1, std::atoi(e));
+        std::vector<int4> it;
+        for (int c = 0; c < nch; ++c) {
+            const int zb = (int)((long long)L.n[2] * c / nch), ze = (int)((long long)L.n[2] * (c + 1) / nch);
+            if (ze <= zb) continue;
+            for (int y = 0; y < ty; ++y)
+                for (int x = 0; x < tx; ++x) it.push_back(make_int4(x, y, zb, ze));
+        }
+        nitems = (int)it.size();
+        items.upload(it.data(), it.size(), s);
+        ctr.alloc_zero(4, s);
+        grid_v = std::min(nitems, sms * ov);
+        grid_p = std::min(nitems, sms * op);
+    }
+
+    void launch(bool velocity, vdk::VdFastParams P, cudaStream_t s) {
+        P.items = items.ptr;
+        P.wq.nitems = nitems;
+        if (velocity) {
+            P.wq.ctr = ctr.ptr;
+            vdk::k_vdv<R><<<grid_v, C::NT, C::SMEM_V, s>>>(tm_p, P);
+        } else {
+            P.wq.ctr = ctr.ptr + 2;
+            vdk::k_vdp<R><<<grid_p, C::NT, C::SMEM_P, s>>>(tm_vx, tm_vy, tm_vz, P);
+        }
+        note_launches(1);
+        MM_CUDA(cudaGetLastError());
+    }
+};
+
+struct FastVdAny {
+    virtual ~FastVdAny() = default;
+    virtual void launch(bool velocity, const vdk::VdFastParams& P, cudaStream_t s) = 0;
+};
+template <int R>
+struct FastVdR : FastVdAny {
+    FastVd<R> f;
+    FastVdR(const Layout& L, float* p, float* const v[3], int dev, cudaStream_t s)
+        : f(L, p, v, dev, s) {}
+    void launch(bool velocity, const vdk::VdFastParams& P, cudaStream_t s) override {
+        f.launch(velocity, P, s);
+    }
+};
+
+std::unique_ptr<FastVdAny> make_fast_vd(const Layout& L, float* p, float* const v[3], int dev,
+                                        cudaStream_t s) {
+    switch (L.r) {
+#define MM_VD_FAST(RR) \
+    case RR:           \
+        return std::make_unique<FastVdR<RR>>(L, p, v, dev, s);
+        MM_VD_FAST(1)
+        MM_VD_FAST(2)
+        MM_VD_FAST(3)
+        MM_VD_FAST(4)
+        MM_VD_FAST(5)
+        MM_VD_FAST(6)
+        MM_VD_FAST(7)
+        MM_VD_FAST(8)
+#undef MM_VD_FAST
+        default:
+            return nullptr;
+    }
+}
+
 }  // namespace vd
 }  // namespace mmb
 
@@ -231,6 +326,7 @@ struct mm_vd_engine {
     DevBuf<float> amps;
     long long steps = 0;
     int zc = 32;
+    std::unique_ptr<vd::FastVdAny> fast;  // null: the plain kernels (MM_VD_SIMPLE)
 
     vd::VdParams params(bool velocity) const {
         vd::VdParams s;
@@ -302,8 +398,38 @@ struct mm_vd_engine {
         return lay.off(src[0], src[1], src[2]);
     }
 
-    void velocity() { vd::launch(true, params(true), stream); }
-    void pressure() { vd::launch(false, params(false), stream); }
+    vdk::VdFastParams fast_params(bool velocity) const {
+        vdk::VdFastParams f;
+        std::memset(&f, 0, sizeof f);
+        const vd::VdParams s = params(velocity);
+        f.lay = s.lay;
+        f.p = s.p;
+        f.ir = s.ir;
+        f.dtb = s.dtb;
+        for (int a = 0; a < 3; ++a) {
+            f.nd[a] = s.nd[a];
+            f.v[a] = s.v[a];
+            f.tab.ta[a] = s.ta[a];
+            f.tab.tb[a] = s.tb[a];
+            f.tab.tik[a] = s.tik[a];
+            for (int m = 0; m < kMaxR; ++m) f.w[a][m] = s.w[a][m];
+            f.run[a][0] = s.run[a][0];
+            f.run[a][1] = s.run[a][1];
+        }
+        return f;
+    }
+    void velocity() {
+        if (fast)
+            fast->launch(true, fast_params(true), stream);
+        else
+            vd::launch(true, params(true), stream);
+    }
+    void pressure() {
+        if (fast)
+            fast->launch(false, fast_params(false), stream);
+        else
+            vd::launch(false, params(false), stream);
+    }
     void inject(float amp, const int* src, const float* amp_dev, const int* step_dev) {
         launch_inject(p.ptr, dtb.ptr, src_off(src), amp, amp_dev, step_dev, stream);
     }
@@ -458,6 +584,10 @@ int mm_vd_create(const mm_grid* grid, const float* vp, const float* rho,
     e->setup_cpml();
     e->counters.alloc_zero(2, e->stream);
     if (const char* zc = std::getenv("MM_VD_ZC")) e->zc = std::max(1, std::atoi(zc));
+    if (!std::getenv("MM_VD_SIMPLE")) {
+        float* const vv[3] = {e->v[0].ptr, e->v[1].ptr, e->v[2].ptr};
+        e->fast = vd::make_fast_vd(e->lay, e->p.ptr, vv, device, e->stream);
+    }
     MM_CUDA(cudaStreamSynchronize(e->stream));
     *out = e.release();
     MM_API_END

@@ -1,0 +1,455 @@
+// vd_fast.cuh -- TMA-fed z-streaming kernels of the acoustic_iso engine.
+//
+// ref: AcousticVdEngine::update_velocity / update_pressure
+// (propagator_impl.hpp:214-273), staggered_derivative_at (stencil.hpp:103-111).
+//
+// Both kernels are persistent (one CTA per resident slot) and pull
+// (x-y tile, z-chunk) items from a work queue ordered chunk-major, so the
+// items in flight are neighbouring tiles at the same depth and their halos
+// meet in L2.  A tile is 32 x 32 points; a thread owns 4 consecutive x points
+// (one float4) of one row.
+//  * k_vdv (velocity): p planes with their x-y halo arrive by TMA into a ring
+//    of NS = 2R + lead slots that holds the whole z window; every neighbour
+//    of the staggered forward derivative is a shared-memory load.
+//  * k_vdp (pressure): vz tiles stream through a ring the same way (z
+//    window); vx with its x halo and vy with its y halo arrive per plane in a
+//    two-stage ring.
+//  * point-wise streams (dt/rho, v in k_vdv; dt*bulk, p in k_vdp) are read
+//    with 16-byte loads one plane ahead into registers and written back with
+//    16-byte stores; CPML memory (the damping-layer runs) likewise.
+//  * thread 0 issues the TMA loads after the per-plane barrier.
+// Arithmetic: the reference's association order, every operation rounded
+// separately (__fadd_rn / __fmul_rn): bit-identical to the CPU reference.
+#pragma once
+
+#include "fast_common.cuh"
+
+namespace mmb {
+namespace vdk {
+
+using fast::comp;
+using fast::lds4;
+using fast::pad32;
+using fast::smem_u32;
+
+__device__ __forceinline__ float fa(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fs(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
+
+template <int R>
+struct VdCfg {
+    static constexpr int TXT = 8;          // threads per row, 4 x-points each
+    static constexpr int TX = 4 * TXT;     // 32
+    static constexpr int TY = 32;          // rows (one per thread row)
+    static constexpr int NT = TXT * TY;    // 256
+    static constexpr int HX = R <= 4 ? 4 : 8;  // x halo (float4 granules)
+    static constexpr int BX = TX + 2 * HX;
+    static constexpr int BY = TY + 2 * R;
+    static constexpr int TILE = pad32(TX * TY);
+    // velocity: p halo planes, ring = z window 2R + lead
+    static constexpr int PPLANE = pad32(BX * BY);
+    static constexpr int NSV = 2 * R + (R <= 4 ? 2 : 1);
+    // pressure: vz tiles (z window 2R + lead), vx / vy halo boxes (NQ stages)
+    static constexpr int NSP = 2 * R + 2;
+    static constexpr int NQP = 2;
+    static constexpr int VXB = pad32(BX * TY), VYB = pad32(TX * BY);
+    static constexpr size_t SMEM_V = sizeof(float) * (size_t)NSV * PPLANE + 8 * NSV + 16;
+    static constexpr size_t SMEM_P =
+        sizeof(float) * (size_t)(NSP * TILE + NQP * (VXB + VYB)) + 8 * (NSP + NQP) + 16;
+};
+
+struct VdTables {
+    const float* ta[3];
+    const float* tb[3];
+    const float* tik[3];
+};
+
+struct VdFastParams {
+    Layout lay;
+    int nd[3];
+    float* p;
+    float* v[3];
+    const float* ir;   // dt / rho
+    const float* dtb;  // dt * ((rho * vp) * vp)
+    float w[3][kMaxR];
+    VdTables tab;
+    CpmlRun run[3][2];  // psi of this pass
+    const int4* items;  // (tile_x, tile_y, z_begin, z_end)
+    fast::WorkQueue wq;
+};
+
+// One thread's 4 points: masks and CPML tables of the item.
+struct PointSet {
+    int xg, y;
+    bool ok[4], all, any;
+    float xa[4], xb[4], xk[4], ya, yb, yk;
+};
+
+// CPML on the 4 terms d[e] of axis `ax` (propagator_impl.hpp:231-238 /
+// :260-267): psi = b psi + a d; d = d ik + psi.  psi lives in the run that
+// holds the point (zero and unstored elsewhere, see vd_engine.cu).
+template <int AX>
+__device__ __forceinline__ void cpml4(float (&d)[4], const CpmlRun (&run)[2], const PointSet& S,
+                                      int k, const float (&a)[4], const float (&b)[4],
+                                      const float (&ik)[4]) {
+    float old[4] = {0.f, 0.f, 0.f, 0.f};
+    float* ps[4] = {nullptr, nullptr, nullptr, nullptr};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int c = AX == 0 ? S.xg + e : AX == 1 ? S.y : k;
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd)
+            if (S.ok[e] && c >= run[sd].lo && c < run[sd].hi)
+                ps[e] = run[sd].psi + run_off(run[sd], AX, S.xg + e, S.y, k);
+        if (ps[e]) old[e] = *ps[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float psi = fa(fm(b[e], old[e]), fm(a[e], d[e]));
+        if (ps[e]) *ps[e] = psi;
+        d[e] = fa(fm(d[e], ik[e]), psi);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void point_set(PointSet& S, const VdFastParams& P, int x0, int y0,
+                                          int tx, int ty) {
+    const Layout& L = P.lay;
+    S.xg = x0 + 4 * tx;
+    S.y = y0 + ty;
+    const bool yok = S.y < L.n[1];
+    S.all = yok;
+    S.any = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        S.ok[e] = yok && S.xg + e < L.n[0];
+        S.all = S.all && S.ok[e];
+        S.any = S.any || S.ok[e];
+        const int xc = min(S.xg + e, L.n[0] - 1);
+        S.xa[e] = __ldg(P.tab.ta[0] + xc);
+        S.xb[e] = __ldg(P.tab.tb[0] + xc);
+        S.xk[e] = __ldg(P.tab.tik[0] + xc);
+    }
+    const int yc = min(S.y, L.n[1] - 1);
+    S.ya = __ldg(P.tab.ta[1] + yc);
+    S.yb = __ldg(P.tab.tb[1] + yc);
+    S.yk = __ldg(P.tab.tik[1] + yc);
+}
+
+// Damping-box membership of the 4 points at depth k (grid.cpp:24-45): outside
+// the inner box.
+__device__ __forceinline__ bool any_damp(const VdFastParams& P, const PointSet& S, int k) {
+    const Layout& L = P.lay;
+    const bool yz_in = S.y >= P.nd[1] && S.y < L.n[1] - P.nd[1] && k >= P.nd[2] &&
+                       k < L.n[2] - P.nd[2];
+    return !(yz_in && S.xg >= P.nd[0] && S.xg + 3 < L.n[0] - P.nd[0]);
+}
+
+// The three CPML terms on points that lie in a damping box (all 4 points of a
+// thread share y and k; along x the box edge may split them).
+__device__ __forceinline__ void cpml_all(float (&d)[3][4], const VdFastParams& P,
+                                         const PointSet& S, int k) {
+    const Layout& L = P.lay;
+    const bool yz_in = S.y >= P.nd[1] && S.y < L.n[1] - P.nd[1] && k >= P.nd[2] &&
+                       k < L.n[2] - P.nd[2];
+    bool damp[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        damp[e] = !(yz_in && S.xg + e >= P.nd[0] && S.xg + e < L.n[0] - P.nd[0]);
+    float dd[3][4];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dd[a][e] = d[a][e];
+    const float ya[4] = {S.ya, S.ya, S.ya, S.ya}, yb[4] = {S.yb, S.yb, S.yb, S.yb},
+                yk[4] = {S.yk, S.yk, S.yk, S.yk};
+    const float za = __ldg(P.tab.ta[2] + k), zb = __ldg(P.tab.tb[2] + k),
+                zk = __ldg(P.tab.tik[2] + k);
+    const float zaa[4] = {za, za, za, za}, zbb[4] = {zb, zb, zb, zb}, zkk[4] = {zk, zk, zk, zk};
+    cpml4<0>(dd[0], P.run[0], S, k, S.xa, S.xb, S.xk);
+    cpml4<1>(dd[1], P.run[1], S, k, ya, yb, yk);
+    cpml4<2>(dd[2], P.run[2], S, k, zaa, zbb, zkk);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (damp[e]) d[a][e] = dd[a][e];
+}
+
+__device__ __forceinline__ float4 ld4z(const float* p, const PointSet& S) {
+    return fast::ld4(p, S.ok, S.all);
+}
+__device__ __forceinline__ void st4v(float* p, const float (&v)[4], const PointSet& S) {
+    fast::st4(p, v, S.ok, S.all);
+}
+
+// ----------------------------------------------------------------- velocity
+template <int R>
+__global__ void __launch_bounds__(VdCfg<R>::NT, 2)
+    k_vdv(const __grid_constant__ CUtensorMap tm_p, const VdFastParams P) {
+    using C = VdCfg<R>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + C::NSV * C::PPLANE);
+    const uint32_t bar0 = smem_u32(bars);
+    const int tid = threadIdx.x;
+    const int tx = tid % C::TXT, ty = tid / C::TXT;
+    const Layout L = P.lay;
+    if (tid == 0) {
+        fast::prefetch_tmap(&tm_p);
+        for (int s = 0; s < C::NSV; ++s) fast::mbar_init(bar0 + 8 * s, 1);
+        fast::fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t ph = 0;  // parity bit per slot
+    __shared__ int s_item;
+    const int soff = (R + ty) * C::BX + C::HX + 4 * tx;
+
+    for (;;) {
+        const int item = fast::wq_next(P.wq, &s_item);
+        if (item >= P.wq.nitems) break;
+        const int4 it = P.items[item];
+        const int x0 = it.x * C::TX, y0 = it.y * C::TY, zb = it.z, ze = it.w;
+        const int nout = ze - zb;
+        const int nring = nout + 2 * R - 1;  // planes zb-R+1 .. ze+R-1
+        auto issue = [&](int j) {
+            const int s = j % C::NSV;
+            const uint32_t bar = bar0 + 8 * s;
+            fast::mbar_expect_tx(bar, 4u * C::BX * C::BY);
+            fast::tma_load_3d(smem_u32(ring + s * C::PPLANE), &tm_p, L.L + x0 - C::HX,
+                              y0 - R + L.r, zb - R + 1 + j + L.r, bar);
+        };
+        if (tid == 0)
+            for (int j = 0; j < min(C::NSV, nring); ++j) issue(j);
+        PointSet S;
+        point_set<R>(S, P, x0, y0, tx, ty);
+        const long long o0 = L.off(S.xg, S.y, zb);
+        // point-wise streams, one plane ahead
+        float4 cir, cv[3], nir = make_float4(0.f, 0.f, 0.f, 0.f), nv[3];
+        if (S.any) {
+            cir = ld4z(P.ir + o0, S);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) cv[a] = ld4z(P.v[a] + o0, S);
+        }
+        for (int j = 0; j < 2 * R - 1; ++j) {
+            fast::mbar_wait(bar0 + 8 * (j % C::NSV), (ph >> (j % C::NSV)) & 1u);
+            ph ^= 1u << (j % C::NSV);
+        }
+        for (int o = 0; o < nout; ++o) {
+            const int k = zb + o;
+            const long long oo = o0 + (long long)o * L.plane;
+            if (S.any && o + 1 < nout) {
+                nir = ld4z(P.ir + oo + L.plane, S);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) nv[a] = ld4z(P.v[a] + oo + L.plane, S);
+            }
+            const int jn = o + 2 * R - 1;  // newest plane of the window
+            fast::mbar_wait(bar0 + 8 * (jn % C::NSV), (ph >> (jn % C::NSV)) & 1u);
+            ph ^= 1u << (jn % C::NSV);
+            const int c = (o + R - 1) % C::NSV;  // slot of plane k
+            const float* Sc = ring + c * C::PPLANE + soff;
+            float d[3][4];
+            // x: t += c_m (p[x+m] - p[x+1-m])
+            {
+                float xs[4 + 2 * C::HX];
+#pragma unroll
+                for (int h = 0; h < (4 + 2 * C::HX) / 4; ++h) {
+                    const float4 v = lds4(Sc - C::HX + 4 * h);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) xs[4 * h + e] = comp(v, e);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float t = 0.0f;
+#pragma unroll
+                    for (int m = 1; m <= R; ++m)
+                        t = fa(t, fm(P.w[0][m - 1], fs(xs[C::HX + e + m], xs[C::HX + e + 1 - m])));
+                    d[0][e] = t;
+                }
+            }
+            // y: rows y+m and y+1-m
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[1][e] = d[2][e] = 0.0f;
+#pragma unroll
+            for (int m = 1; m <= R; ++m) {
+                const float4 u = lds4(Sc + m * C::BX), dn = lds4(Sc + (1 - m) * C::BX);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    d[1][e] = fa(d[1][e], fm(P.w[1][m - 1], fs(comp(u, e), comp(dn, e))));
+            }
+            // z: planes k+m <-> ring plane o+R-1+m, k+1-m <-> o+R-m
+#pragma unroll
+            for (int m = 1; m <= R; ++m) {
+                const float4 u = lds4(ring + ((o + R - 1 + m) % C::NSV) * C::PPLANE + soff);
+                const float4 dn = lds4(ring + ((o + R - m) % C::NSV) * C::PPLANE + soff);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    d[2][e] = fa(d[2][e], fm(P.w[2][m - 1], fs(comp(u, e), comp(dn, e))));
+            }
+            if (S.any) {
+                if (any_damp(P, S, k)) cpml_all(d, P, S, k);
+                float out[3][4];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) out[a][e] = fa(comp(cv[a], e), fm(comp(cir, e), d[a][e]));
+#pragma unroll
+                for (int a = 0; a < 3; ++a) st4v(P.v[a] + oo, out[a], S);
+                cir = nir;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) cv[a] = nv[a];
+            }
+            __syncthreads();  // plane o (the window's oldest) is free
+            if (tid == 0 && o + C::NSV < nring) issue(o + C::NSV);
+        }
+        // planes issued but not consumed as "newest": none (the loop waited on
+        // every plane up to nring - 1)
+    }
+    fast::wq_done(P.wq);
+}
+
+// ----------------------------------------------------------------- pressure
+template <int R>
+__global__ void __launch_bounds__(VdCfg<R>::NT, 2)
+    k_vdp(const __grid_constant__ CUtensorMap tm_vx, const __grid_constant__ CUtensorMap tm_vy,
+          const __grid_constant__ CUtensorMap tm_vz, const VdFastParams P) {
+    using C = VdCfg<R>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    float* qring = ring + C::NSP * C::TILE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(qring + C::NQP * (C::VXB + C::VYB));
+    const uint32_t barZ = smem_u32(bars), barQ = smem_u32(bars + C::NSP);
+    const int tid = threadIdx.x;
+    const int tx = tid % C::TXT, ty = tid / C::TXT;
+    const Layout L = P.lay;
+    if (tid == 0) {
+        fast::prefetch_tmap(&tm_vx);
+        fast::prefetch_tmap(&tm_vy);
+        fast::prefetch_tmap(&tm_vz);
+        for (int s = 0; s < C::NSP + C::NQP; ++s) fast::mbar_init(barZ + 8 * s, 1);
+        fast::fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t phZ = 0, phQ = 0;
+    unsigned qn = 0;  // stages consumed (all threads), == stages issued - NQP in flight
+    __shared__ int s_item;
+    const int toff = ty * C::TX + 4 * tx;
+    const int xoff = ty * C::BX + C::HX + 4 * tx;  // in a vx box
+    const int yoff = (R + ty) * C::TX + 4 * tx;    // in a vy box
+
+    for (;;) {
+        const int item = fast::wq_next(P.wq, &s_item);
+        if (item >= P.wq.nitems) break;
+        const int4 it = P.items[item];
+        const int x0 = it.x * C::TX, y0 = it.y * C::TY, zb = it.z, ze = it.w;
+        const int nout = ze - zb;
+        const int nring = nout + 2 * R - 1;  // vz planes zb-R .. ze+R-2
+        auto issue_z = [&](int j) {
+            const int s = j % C::NSP;
+            const uint32_t bar = barZ + 8 * s;
+            fast::mbar_expect_tx(bar, 4u * C::TX * C::TY);
+            fast::tma_load_3d(smem_u32(ring + s * C::TILE), &tm_vz, L.L + x0, y0 + L.r,
+                              zb - R + j + L.r, bar);
+        };
+        const unsigned qbase = qn;
+        auto issue_q = [&](int o) {
+            const int st = (qbase + o) % C::NQP;
+            const uint32_t bar = barQ + 8 * st;
+            float* dst = qring + st * (C::VXB + C::VYB);
+            fast::mbar_expect_tx(bar, 4u * (C::BX * C::TY + C::TX * C::BY));
+            fast::tma_load_3d(smem_u32(dst), &tm_vx, L.L + x0 - C::HX, y0 + L.r, zb + o + L.r, bar);
+            fast::tma_load_3d(smem_u32(dst + C::VXB), &tm_vy, L.L + x0, y0 - R + L.r,
+                              zb + o + L.r, bar);
+        };
+        if (tid == 0) {
+            for (int j = 0; j < min(C::NSP, nring); ++j) issue_z(j);
+            for (int o = 0; o < min(C::NQP, nout); ++o) issue_q(o);
+        }
+        PointSet S;
+        point_set<R>(S, P, x0, y0, tx, ty);
+        const long long o0 = L.off(S.xg, S.y, zb);
+        float4 cdt, cp, ndt = make_float4(0.f, 0.f, 0.f, 0.f), np_ = ndt;
+        if (S.any) {
+            cdt = ld4z(P.dtb + o0, S);
+            cp = ld4z(P.p + o0, S);
+        }
+        for (int j = 0; j < 2 * R - 1; ++j) {
+            fast::mbar_wait(barZ + 8 * (j % C::NSP), (phZ >> (j % C::NSP)) & 1u);
+            phZ ^= 1u << (j % C::NSP);
+        }
+        for (int o = 0; o < nout; ++o) {
+            const int k = zb + o;
+            const long long oo = o0 + (long long)o * L.plane;
+            if (S.any && o + 1 < nout) {
+                ndt = ld4z(P.dtb + oo + L.plane, S);
+                np_ = ld4z(P.p + oo + L.plane, S);
+            }
+            const int jn = o + 2 * R - 1;
+            fast::mbar_wait(barZ + 8 * (jn % C::NSP), (phZ >> (jn % C::NSP)) & 1u);
+            phZ ^= 1u << (jn % C::NSP);
+            const int st = qn % C::NQP;
+            fast::mbar_wait(barQ + 8 * st, (phQ >> st) & 1u);
+            phQ ^= 1u << st;
+            const float* Q = qring + st * (C::VXB + C::VYB);
+            float d[3][4];
+            // x: t += c_m (vx[x+m-1] - vx[x-m])
+            {
+                float xs[4 + 2 * C::HX];
+#pragma unroll
+                for (int h = 0; h < (4 + 2 * C::HX) / 4; ++h) {
+                    const float4 v = lds4(Q + xoff - C::HX + 4 * h);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) xs[4 * h + e] = comp(v, e);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float t = 0.0f;
+#pragma unroll
+                    for (int m = 1; m <= R; ++m)
+                        t = fa(t, fm(P.w[0][m - 1], fs(xs[C::HX + e + m - 1], xs[C::HX + e - m])));
+                    d[0][e] = t;
+                }
+            }
+            // y: rows y+m-1 and y-m
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[1][e] = d[2][e] = 0.0f;
+#pragma unroll
+            for (int m = 1; m <= R; ++m) {
+                const float4 u = lds4(Q + C::VXB + yoff + (m - 1) * C::TX);
+                const float4 dn = lds4(Q + C::VXB + yoff - m * C::TX);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    d[1][e] = fa(d[1][e], fm(P.w[1][m - 1], fs(comp(u, e), comp(dn, e))));
+            }
+            // z: planes k+m-1 <-> ring plane o+R+m-1, k-m <-> o+R-m
+#pragma unroll
+            for (int m = 1; m <= R; ++m) {
+                const float4 u = lds4(ring + ((o + R + m - 1) % C::NSP) * C::TILE + toff);
+                const float4 dn = lds4(ring + ((o + R - m) % C::NSP) * C::TILE + toff);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    d[2][e] = fa(d[2][e], fm(P.w[2][m - 1], fs(comp(u, e), comp(dn, e))));
+            }
+            ++qn;
+            if (S.any) {
+                if (any_damp(P, S, k)) cpml_all(d, P, S, k);
+                float out[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    out[e] = fa(comp(cp, e), fm(comp(cdt, e), fa(fa(d[0][e], d[1][e]), d[2][e])));
+                st4v(P.p + oo, out, S);
+                cdt = ndt;
+                cp = np_;
+            }
+            __syncthreads();  // vz plane o and stage o are free
+            if (tid == 0) {
+                if (o + C::NSP < nring) issue_z(o + C::NSP);
+                if (o + C::NQP < nout) issue_q(o + C::NQP);
+            }
+        }
+    }
+    fast::wq_done(P.wq);
+}
+
+}  // namespace vdk
+}  // namespace mmb
