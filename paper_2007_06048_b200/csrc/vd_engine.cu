@@ -365,21 +365,23 @@ struct mm_vd_engine {
                 vrun[ax][side] = prun[ax][side] = r;
                 if (hi_[side] <= lo_[side] || !active) continue;
                 const long long wdt = hi_[side] - lo_[side];
+                const long long nx4 = (lay.n[0] + 3) / 4 * 4;
                 r.lo = lo_[side];
                 r.hi = hi_[side];
-                r.org = r.lo;
+                // rows start 16-byte aligned so the fast kernels move psi as float4
+                r.org = ax == 0 ? (r.lo & ~3) : r.lo;
                 size_t count;
                 if (ax == 0) {
-                    r.s1 = wdt;
-                    r.s2 = wdt * lay.n[1];
+                    r.s1 = (r.hi - r.org + 3) / 4 * 4;
+                    r.s2 = r.s1 * lay.n[1];
                     count = (size_t)r.s2 * lay.n[2];
                 } else if (ax == 1) {
-                    r.s1 = lay.n[0];
-                    r.s2 = (long long)lay.n[0] * wdt;
+                    r.s1 = nx4;
+                    r.s2 = nx4 * wdt;
                     count = (size_t)r.s2 * lay.n[2];
                 } else {
-                    r.s1 = lay.n[0];
-                    r.s2 = (long long)lay.n[0] * lay.n[1];
+                    r.s1 = nx4;
+                    r.s2 = nx4 * lay.n[1];
                     count = (size_t)r.s2 * wdt;
                 }
                 vpsi[ax][side].alloc_zero(count, stream);

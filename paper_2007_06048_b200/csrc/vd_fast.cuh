@@ -78,42 +78,46 @@ struct VdFastParams {
     fast::WorkQueue wq;
 };
 
-// One thread's 4 points: masks and CPML tables of the item.
+// CPML memory of one axis for one thread's 4 points: the run array element
+// of point 0 at the item's first plane, the per-plane step, and which of the
+// 4 points lie in the run.
+struct RunPtr {
+    float* p;  // nullptr: no point of the thread in this run
+    long long step;
+    bool on[4];
+    bool all;
+};
+
+// One thread's 4 points: masks, CPML tables and run pointers of the item.
 struct PointSet {
     int xg, y;
     bool ok[4], all, any;
     float xa[4], xb[4], xk[4], ya, yb, yk;
+    RunPtr rx[2], ry;
 };
 
-// CPML on the 4 terms d[e] of axis `ax` (propagator_impl.hpp:231-238 /
-// :260-267): psi = b psi + a d; d = d ik + psi.  psi lives in the run that
-// holds the point (zero and unstored elsewhere, see vd_engine.cu).
-template <int AX>
-__device__ __forceinline__ void cpml4(float (&d)[4], const CpmlRun (&run)[2], const PointSet& S,
-                                      int k, const float (&a)[4], const float (&b)[4],
-                                      const float (&ik)[4]) {
-    float old[4] = {0.f, 0.f, 0.f, 0.f};
-    float* ps[4] = {nullptr, nullptr, nullptr, nullptr};
+__device__ __forceinline__ void run_ptr(RunPtr& rp, const CpmlRun& r, int ax, int xg, int y,
+                                        int zb, const bool (&ok)[4]) {
+    rp.p = nullptr;
+    rp.step = 0;
+    rp.all = true;
+    bool any = false;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        const int c = AX == 0 ? S.xg + e : AX == 1 ? S.y : k;
-#pragma unroll
-        for (int sd = 0; sd < 2; ++sd)
-            if (S.ok[e] && c >= run[sd].lo && c < run[sd].hi)
-                ps[e] = run[sd].psi + run_off(run[sd], AX, S.xg + e, S.y, k);
-        if (ps[e]) old[e] = *ps[e];
+        const int c = ax == 0 ? xg + e : y;
+        rp.on[e] = ok[e] && c >= r.lo && c < r.hi;
+        any = any || rp.on[e];
+        rp.all = rp.all && rp.on[e];
     }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const float psi = fa(fm(b[e], old[e]), fm(a[e], d[e]));
-        if (ps[e]) *ps[e] = psi;
-        d[e] = fa(fm(d[e], ik[e]), psi);
+    if (any) {
+        rp.p = r.psi + run_off(r, ax, xg, y, zb);
+        rp.step = r.s2;
     }
 }
 
 template <int R>
 __device__ __forceinline__ void point_set(PointSet& S, const VdFastParams& P, int x0, int y0,
-                                          int tx, int ty) {
+                                          int tx, int ty, int zb) {
     const Layout& L = P.lay;
     S.xg = x0 + 4 * tx;
     S.y = y0 + ty;
@@ -134,46 +138,65 @@ __device__ __forceinline__ void point_set(PointSet& S, const VdFastParams& P, in
     S.ya = __ldg(P.tab.ta[1] + yc);
     S.yb = __ldg(P.tab.tb[1] + yc);
     S.yk = __ldg(P.tab.tik[1] + yc);
+    run_ptr(S.rx[0], P.run[0][0], 0, S.xg, S.y, zb, S.ok);
+    run_ptr(S.rx[1], P.run[0][1], 0, S.xg, S.y, zb, S.ok);
+    run_ptr(S.ry, P.run[1][0], 1, S.xg, S.y, zb, S.ok);
+    if (!S.ry.p) run_ptr(S.ry, P.run[1][1], 1, S.xg, S.y, zb, S.ok);
 }
 
-// Damping-box membership of the 4 points at depth k (grid.cpp:24-45): outside
-// the inner box.
-__device__ __forceinline__ bool any_damp(const VdFastParams& P, const PointSet& S, int k) {
-    const Layout& L = P.lay;
-    const bool yz_in = S.y >= P.nd[1] && S.y < L.n[1] - P.nd[1] && k >= P.nd[2] &&
-                       k < L.n[2] - P.nd[2];
-    return !(yz_in && S.xg >= P.nd[0] && S.xg + 3 < L.n[0] - P.nd[0]);
-}
-
-// The three CPML terms on points that lie in a damping box (all 4 points of a
-// thread share y and k; along x the box edge may split them).
-__device__ __forceinline__ void cpml_all(float (&d)[3][4], const VdFastParams& P,
-                                         const PointSet& S, int k) {
-    const Layout& L = P.lay;
-    const bool yz_in = S.y >= P.nd[1] && S.y < L.n[1] - P.nd[1] && k >= P.nd[2] &&
-                       k < L.n[2] - P.nd[2];
-    bool damp[4];
+// CPML on the terms of the points in one run (propagator_impl.hpp:231-238 /
+// :260-267): psi = b psi + a d; d = d ik + psi.  Points outside every run of
+// an axis have a = 0, b = ik = 1 there: their psi stays +0 and d is unchanged
+// for the update (v and p never hold -0), so they are skipped (vd_engine.cu).
+__device__ __forceinline__ void cpml_run(float (&d)[4], float* ps, const bool (&on)[4], bool all,
+                                         const float (&a)[4], const float (&b)[4],
+                                         const float (&ik)[4]) {
+    float old[4];
+    if (all) {
+        const float4 v = *reinterpret_cast<const float4*>(ps);
+        old[0] = v.x, old[1] = v.y, old[2] = v.z, old[3] = v.w;
+    } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-        damp[e] = !(yz_in && S.xg + e >= P.nd[0] && S.xg + e < L.n[0] - P.nd[0]);
-    float dd[3][4];
+        for (int e = 0; e < 4; ++e) old[e] = on[e] ? ps[e] : 0.0f;
+    }
+    float nw[4];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) dd[a][e] = d[a][e];
-    const float ya[4] = {S.ya, S.ya, S.ya, S.ya}, yb[4] = {S.yb, S.yb, S.yb, S.yb},
-                yk[4] = {S.yk, S.yk, S.yk, S.yk};
-    const float za = __ldg(P.tab.ta[2] + k), zb = __ldg(P.tab.tb[2] + k),
-                zk = __ldg(P.tab.tik[2] + k);
-    const float zaa[4] = {za, za, za, za}, zbb[4] = {zb, zb, zb, zb}, zkk[4] = {zk, zk, zk, zk};
-    cpml4<0>(dd[0], P.run[0], S, k, S.xa, S.xb, S.xk);
-    cpml4<1>(dd[1], P.run[1], S, k, ya, yb, yk);
-    cpml4<2>(dd[2], P.run[2], S, k, zaa, zbb, zkk);
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
+    for (int e = 0; e < 4; ++e) {
+        nw[e] = fa(fm(b[e], old[e]), fm(a[e], d[e]));
+        if (on[e]) d[e] = fa(fm(d[e], ik[e]), nw[e]);
+    }
+    if (all) {
+        *reinterpret_cast<float4*>(ps) = make_float4(nw[0], nw[1], nw[2], nw[3]);
+    } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-            if (damp[e]) d[a][e] = dd[a][e];
+            if (on[e]) ps[e] = nw[e];
+    }
+}
+
+// All CPML terms of the thread's 4 points at output plane o (depth k).
+__device__ __forceinline__ void cpml_plane(float (&d)[3][4], const VdFastParams& P,
+                                           const PointSet& S, int o, int k) {
+#pragma unroll
+    for (int sd = 0; sd < 2; ++sd)
+        if (S.rx[sd].p)
+            cpml_run(d[0], S.rx[sd].p + o * S.rx[sd].step, S.rx[sd].on, S.rx[sd].all, S.xa,
+                     S.xb, S.xk);
+    if (S.ry.p) {
+        const float a[4] = {S.ya, S.ya, S.ya, S.ya}, b[4] = {S.yb, S.yb, S.yb, S.yb},
+                    ik[4] = {S.yk, S.yk, S.yk, S.yk};
+        cpml_run(d[1], S.ry.p + o * S.ry.step, S.ry.on, S.ry.all, a, b, ik);
+    }
+#pragma unroll
+    for (int sd = 0; sd < 2; ++sd) {
+        const CpmlRun& r = P.run[2][sd];
+        if (S.any && k >= r.lo && k < r.hi) {
+            const float za = __ldg(P.tab.ta[2] + k), zb = __ldg(P.tab.tb[2] + k),
+                        zk = __ldg(P.tab.tik[2] + k);
+            const float a[4] = {za, za, za, za}, b[4] = {zb, zb, zb, zb}, ik[4] = {zk, zk, zk, zk};
+            cpml_run(d[2], r.psi + run_off(r, 2, S.xg, S.y, k), S.ok, S.all, a, b, ik);
+        }
+    }
 }
 
 __device__ __forceinline__ float4 ld4z(const float* p, const PointSet& S) {
@@ -222,7 +245,7 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
         if (tid == 0)
             for (int j = 0; j < min(C::NSV, nring); ++j) issue(j);
         PointSet S;
-        point_set<R>(S, P, x0, y0, tx, ty);
+        point_set<R>(S, P, x0, y0, tx, ty, zb);
         const long long o0 = L.off(S.xg, S.y, zb);
         // point-wise streams, one plane ahead
         float4 cir, cv[3], nir = make_float4(0.f, 0.f, 0.f, 0.f), nv[3];
@@ -287,7 +310,7 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
                     d[2][e] = fa(d[2][e], fm(P.w[2][m - 1], fs(comp(u, e), comp(dn, e))));
             }
             if (S.any) {
-                if (any_damp(P, S, k)) cpml_all(d, P, S, k);
+                cpml_plane(d, P, S, o, k);
                 float out[3][4];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
@@ -366,7 +389,7 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
             for (int o = 0; o < min(C::NQP, nout); ++o) issue_q(o);
         }
         PointSet S;
-        point_set<R>(S, P, x0, y0, tx, ty);
+        point_set<R>(S, P, x0, y0, tx, ty, zb);
         const long long o0 = L.off(S.xg, S.y, zb);
         float4 cdt, cp, ndt = make_float4(0.f, 0.f, 0.f, 0.f), np_ = ndt;
         if (S.any) {
@@ -432,7 +455,7 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
             }
             ++qn;
             if (S.any) {
-                if (any_damp(P, S, k)) cpml_all(d, P, S, k);
+                cpml_plane(d, P, S, o, k);
                 float out[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
