@@ -211,16 +211,24 @@ void launch(bool velocity, const VdParams& P, cudaStream_t s) {
 template <int R>
 struct FastVd {
     using C = vdk::VdCfg<R>;
-    CUtensorMap tm_p, tm_vx, tm_vy, tm_vz;
+    vdk::VdvMaps mv;
+    vdk::VdpMaps mp;
     DevBuf<int4> items;
     DevBuf<int> ctr;  // [0..1] velocity queue, [2..3] pressure queue
     int nitems = 0, grid_v = 0, grid_p = 0;
 
-    FastVd(const Layout& L, float* p, float* const v[3], int device, cudaStream_t s) {
-        tm_p = tma_field_map(L, p, C::BX, C::BY);
-        tm_vx = tma_field_map(L, v[0], C::BX, C::TY);
-        tm_vy = tma_field_map(L, v[1], C::TX, C::BY);
-        tm_vz = tma_field_map(L, v[2], C::TX, C::TY);
+    FastVd(const Layout& L, float* p, float* const v[3], const float* ir, const float* dtb,
+           int device, cudaStream_t s) {
+        mv.p = tma_field_map(L, p, C::BX, C::BY);
+        mv.ir = tma_field_map(L, ir, C::TX, C::TY);
+        mv.vx = tma_field_map(L, v[0], C::TX, C::TY);
+        mv.vy = tma_field_map(L, v[1], C::TX, C::TY);
+        mv.vz = tma_field_map(L, v[2], C::TX, C::TY);
+        mp.vx = tma_field_map(L, v[0], C::BX, C::TY);
+        mp.vy = tma_field_map(L, v[1], C::TX, C::BY);
+        mp.vz = mv.vz;
+        mp.dtb = tma_field_map(L, dtb, C::TX, C::TY);
+        mp.p = tma_field_map(L, p, C::TX, C::TY);
         MM_CUDA(cudaFuncSetAttribute(vdk::k_vdv<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)C::SMEM_V));
         MM_CUDA(cudaFuncSetAttribute(vdk::k_vdp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -255,10 +263,10 @@ struct FastVd {
         P.wq.nitems = nitems;
         if (velocity) {
             P.wq.ctr = ctr.ptr;
-            vdk::k_vdv<R><<<grid_v, C::NT, C::SMEM_V, s>>>(tm_p, P);
+            vdk::k_vdv<R><<<grid_v, C::NT, C::SMEM_V, s>>>(mv, P);
         } else {
             P.wq.ctr = ctr.ptr + 2;
-            vdk::k_vdp<R><<<grid_p, C::NT, C::SMEM_P, s>>>(tm_vx, tm_vy, tm_vz, P);
+            vdk::k_vdp<R><<<grid_p, C::NT, C::SMEM_P, s>>>(mp, P);
         }
         note_launches(1);
         MM_CUDA(cudaGetLastError());
@@ -272,19 +280,21 @@ struct FastVdAny {
 template <int R>
 struct FastVdR : FastVdAny {
     FastVd<R> f;
-    FastVdR(const Layout& L, float* p, float* const v[3], int dev, cudaStream_t s)
-        : f(L, p, v, dev, s) {}
+    FastVdR(const Layout& L, float* p, float* const v[3], const float* ir, const float* dtb,
+            int dev, cudaStream_t s)
+        : f(L, p, v, ir, dtb, dev, s) {}
     void launch(bool velocity, const vdk::VdFastParams& P, cudaStream_t s) override {
         f.launch(velocity, P, s);
     }
 };
 
-std::unique_ptr<FastVdAny> make_fast_vd(const Layout& L, float* p, float* const v[3], int dev,
+std::unique_ptr<FastVdAny> make_fast_vd(const Layout& L, float* p, float* const v[3],
+                                        const float* ir, const float* dtb, int dev,
                                         cudaStream_t s) {
     switch (L.r) {
 #define MM_VD_FAST(RR) \
     case RR:           \
-        return std::make_unique<FastVdR<RR>>(L, p, v, dev, s);
+        return std::make_unique<FastVdR<RR>>(L, p, v, ir, dtb, dev, s);
         MM_VD_FAST(1)
         MM_VD_FAST(2)
         MM_VD_FAST(3)
@@ -588,7 +598,7 @@ int mm_vd_create(const mm_grid* grid, const float* vp, const float* rho,
     if (const char* zc = std::getenv("MM_VD_ZC")) e->zc = std::max(1, std::atoi(zc));
     if (!std::getenv("MM_VD_SIMPLE")) {
         float* const vv[3] = {e->v[0].ptr, e->v[1].ptr, e->v[2].ptr};
-        e->fast = vd::make_fast_vd(e->lay, e->p.ptr, vv, device, e->stream);
+        e->fast = vd::make_fast_vd(e->lay, e->p.ptr, vv, e->ir.ptr, e->dtb.ptr, device, e->stream);
     }
     MM_CUDA(cudaStreamSynchronize(e->stream));
     *out = e.release();

@@ -14,9 +14,10 @@
 //  * k_vdp (pressure): vz tiles stream through a ring the same way (z
 //    window); vx with its x halo and vy with its y halo arrive per plane in a
 //    two-stage ring.
-//  * point-wise streams (dt/rho, v in k_vdv; dt*bulk, p in k_vdp) are read
-//    with 16-byte loads one plane ahead into registers and written back with
-//    16-byte stores; CPML memory (the damping-layer runs) likewise.
+//  * point-wise streams (dt/rho, v in k_vdv; dt*bulk, p in k_vdp) arrive by
+//    TMA in a stage ring a few planes ahead and are written back with 16-byte
+//    stores; CPML memory (the damping-layer runs) moves as float4 loads issued
+//    at the top of a plane.
 //  * thread 0 issues the TMA loads after the per-plane barrier.
 // Arithmetic: the reference's association order, every operation rounded
 // separately (__fadd_rn / __fmul_rn): bit-identical to the CPU reference.
@@ -48,14 +49,16 @@ struct VdCfg {
     static constexpr int TILE = pad32(TX * TY);
     // velocity: p halo planes, ring = z window 2R + lead
     static constexpr int PPLANE = pad32(BX * BY);
-    static constexpr int NSV = 2 * R + (R <= 4 ? 2 : 1);
-    // pressure: vz tiles (z window 2R + lead), vx / vy halo boxes (NQ stages)
+    static constexpr int NSV = 2 * R + 1;
+    static constexpr int NQV = R <= 4 ? 3 : 2;  // dt/rho + v stages
+    // pressure: vz tiles (z window 2R + lead), vx / vy halo boxes + dtb + p (NQ stages)
     static constexpr int NSP = 2 * R + 2;
-    static constexpr int NQP = 2;
+    static constexpr int NQP = 3;
     static constexpr int VXB = pad32(BX * TY), VYB = pad32(TX * BY);
-    static constexpr size_t SMEM_V = sizeof(float) * (size_t)NSV * PPLANE + 8 * NSV + 16;
-    static constexpr size_t SMEM_P =
-        sizeof(float) * (size_t)(NSP * TILE + NQP * (VXB + VYB)) + 8 * (NSP + NQP) + 16;
+    static constexpr size_t SMEM_V =
+        sizeof(float) * (size_t)(NSV * PPLANE + NQV * 4 * TILE) + 8 * (NSV + NQV) + 16;
+    static constexpr size_t SMEM_P = sizeof(float) * (size_t)(NSP * TILE + NQP * (VXB + VYB + 2 * TILE)) +
+                                     8 * (NSP + NQP) + 16;
 };
 
 struct VdTables {
@@ -144,27 +147,30 @@ __device__ __forceinline__ void point_set(PointSet& S, const VdFastParams& P, in
     if (!S.ry.p) run_ptr(S.ry, P.run[1][1], 1, S.xg, S.y, zb, S.ok);
 }
 
-// CPML on the terms of the points in one run (propagator_impl.hpp:231-238 /
-// :260-267): psi = b psi + a d; d = d ik + psi.  Points outside every run of
-// an axis have a = 0, b = ik = 1 there: their psi stays +0 and d is unchanged
-// for the update (v and p never hold -0), so they are skipped (vd_engine.cu).
-__device__ __forceinline__ void cpml_run(float (&d)[4], float* ps, const bool (&on)[4], bool all,
-                                         const float (&a)[4], const float (&b)[4],
-                                         const float (&ik)[4]) {
-    float old[4];
+// CPML (propagator_impl.hpp:231-238 / :260-267): psi = b psi + a d;
+// d = d ik + psi, on the points of each damping-layer run.  Points outside
+// every run of an axis have a = 0, b = ik = 1 there: their psi stays +0 and d
+// is unchanged for the update (v and p never hold -0), so they are skipped
+// (see vd_engine.cu).  The old psi values are loaded at the top of a plane
+// (psi_load) so their latency hides behind the stencil; psi_apply finishes.
+struct PsiState {
+    float ox[4], oy[4], oz[4];
+    float* pz;  // z-run element of point 0 at this plane (nullptr: none)
+};
+
+__device__ __forceinline__ void ld_run(float (&old)[4], const float* ps, const bool (&on)[4],
+                                       bool all) {
     if (all) {
         const float4 v = *reinterpret_cast<const float4*>(ps);
         old[0] = v.x, old[1] = v.y, old[2] = v.z, old[3] = v.w;
     } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) old[e] = on[e] ? ps[e] : 0.0f;
+        for (int e = 0; e < 4; ++e)
+            if (on[e]) old[e] = ps[e];
     }
-    float nw[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        nw[e] = fa(fm(b[e], old[e]), fm(a[e], d[e]));
-        if (on[e]) d[e] = fa(fm(d[e], ik[e]), nw[e]);
-    }
+}
+__device__ __forceinline__ void st_run(float* ps, const float (&nw)[4], const bool (&on)[4],
+                                       bool all) {
     if (all) {
         *reinterpret_cast<float4*>(ps) = make_float4(nw[0], nw[1], nw[2], nw[3]);
     } else {
@@ -174,59 +180,98 @@ __device__ __forceinline__ void cpml_run(float (&d)[4], float* ps, const bool (&
     }
 }
 
-// All CPML terms of the thread's 4 points at output plane o (depth k).
-__device__ __forceinline__ void cpml_plane(float (&d)[3][4], const VdFastParams& P,
-                                           const PointSet& S, int o, int k) {
+__device__ __forceinline__ void psi_load(PsiState& st, const VdFastParams& P, const PointSet& S,
+                                         int o, int k) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) st.ox[e] = st.oy[e] = st.oz[e] = 0.0f;
 #pragma unroll
     for (int sd = 0; sd < 2; ++sd)
-        if (S.rx[sd].p)
-            cpml_run(d[0], S.rx[sd].p + o * S.rx[sd].step, S.rx[sd].on, S.rx[sd].all, S.xa,
-                     S.xb, S.xk);
-    if (S.ry.p) {
-        const float a[4] = {S.ya, S.ya, S.ya, S.ya}, b[4] = {S.yb, S.yb, S.yb, S.yb},
-                    ik[4] = {S.yk, S.yk, S.yk, S.yk};
-        cpml_run(d[1], S.ry.p + o * S.ry.step, S.ry.on, S.ry.all, a, b, ik);
-    }
+        if (S.rx[sd].p) ld_run(st.ox, S.rx[sd].p + o * S.rx[sd].step, S.rx[sd].on, S.rx[sd].all);
+    if (S.ry.p) ld_run(st.oy, S.ry.p + o * S.ry.step, S.ry.on, S.ry.all);
+    st.pz = nullptr;
 #pragma unroll
     for (int sd = 0; sd < 2; ++sd) {
         const CpmlRun& r = P.run[2][sd];
-        if (S.any && k >= r.lo && k < r.hi) {
-            const float za = __ldg(P.tab.ta[2] + k), zb = __ldg(P.tab.tb[2] + k),
-                        zk = __ldg(P.tab.tik[2] + k);
-            const float a[4] = {za, za, za, za}, b[4] = {zb, zb, zb, zb}, ik[4] = {zk, zk, zk, zk};
-            cpml_run(d[2], r.psi + run_off(r, 2, S.xg, S.y, k), S.ok, S.all, a, b, ik);
-        }
+        if (S.any && k >= r.lo && k < r.hi) st.pz = r.psi + run_off(r, 2, S.xg, S.y, k);
+    }
+    if (st.pz) ld_run(st.oz, st.pz, S.ok, S.all);
+}
+
+__device__ __forceinline__ void psi_step(float (&d)[4], float (&nw)[4], const float (&old)[4],
+                                         const bool (&on)[4], const float (&a)[4],
+                                         const float (&b)[4], const float (&ik)[4]) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        nw[e] = fa(fm(b[e], old[e]), fm(a[e], d[e]));
+        if (on[e]) d[e] = fa(fm(d[e], ik[e]), nw[e]);
     }
 }
 
-__device__ __forceinline__ float4 ld4z(const float* p, const PointSet& S) {
-    return fast::ld4(p, S.ok, S.all);
+__device__ __forceinline__ void psi_apply(float (&d)[3][4], const PsiState& st,
+                                          const VdFastParams& P, const PointSet& S, int o,
+                                          int k) {
+    float nw[4];
+    if (S.rx[0].p || S.rx[1].p) {
+        bool on[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) on[e] = S.rx[0].on[e] || S.rx[1].on[e];
+        psi_step(d[0], nw, st.ox, on, S.xa, S.xb, S.xk);
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd)
+            if (S.rx[sd].p) st_run(S.rx[sd].p + o * S.rx[sd].step, nw, S.rx[sd].on, S.rx[sd].all);
+    }
+    if (S.ry.p) {
+        const float a[4] = {S.ya, S.ya, S.ya, S.ya}, b[4] = {S.yb, S.yb, S.yb, S.yb},
+                    ik[4] = {S.yk, S.yk, S.yk, S.yk};
+        psi_step(d[1], nw, st.oy, S.ry.on, a, b, ik);
+        st_run(S.ry.p + o * S.ry.step, nw, S.ry.on, S.ry.all);
+    }
+    if (st.pz) {
+        const float za = __ldg(P.tab.ta[2] + k), zb = __ldg(P.tab.tb[2] + k),
+                    zk = __ldg(P.tab.tik[2] + k);
+        const float a[4] = {za, za, za, za}, b[4] = {zb, zb, zb, zb}, ik[4] = {zk, zk, zk, zk};
+        psi_step(d[2], nw, st.oz, S.ok, a, b, ik);
+        st_run(st.pz, nw, S.ok, S.all);
+    }
 }
+
 __device__ __forceinline__ void st4v(float* p, const float (&v)[4], const PointSet& S) {
     fast::st4(p, v, S.ok, S.all);
 }
 
 // ----------------------------------------------------------------- velocity
+// maps: p (BX x BY halo box), dt/rho and vx, vy, vz (TX x TY tiles)
+struct VdvMaps {
+    CUtensorMap p, ir, vx, vy, vz;
+};
+
 template <int R>
 __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
-    k_vdv(const __grid_constant__ CUtensorMap tm_p, const VdFastParams P) {
+    k_vdv(const __grid_constant__ VdvMaps M, const VdFastParams P) {
     using C = VdCfg<R>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + C::NSV * C::PPLANE);
-    const uint32_t bar0 = smem_u32(bars);
+    float* qring = ring + C::NSV * C::PPLANE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(qring + C::NQV * 4 * C::TILE);
+    const uint32_t bar0 = smem_u32(bars), barQ = smem_u32(bars + C::NSV);
     const int tid = threadIdx.x;
     const int tx = tid % C::TXT, ty = tid / C::TXT;
     const Layout L = P.lay;
     if (tid == 0) {
-        fast::prefetch_tmap(&tm_p);
-        for (int s = 0; s < C::NSV; ++s) fast::mbar_init(bar0 + 8 * s, 1);
+        fast::prefetch_tmap(&M.p);
+        fast::prefetch_tmap(&M.ir);
+        fast::prefetch_tmap(&M.vx);
+        fast::prefetch_tmap(&M.vy);
+        fast::prefetch_tmap(&M.vz);
+        for (int s = 0; s < C::NSV + C::NQV; ++s) fast::mbar_init(bar0 + 8 * s, 1);
         fast::fence_barrier_init();
     }
     __syncthreads();
-    uint32_t ph = 0;  // parity bit per slot
+    uint32_t ph = 0, phQ = 0;  // parity bit per slot / stage
+    unsigned qn = 0;           // stages consumed so far
     __shared__ int s_item;
     const int soff = (R + ty) * C::BX + C::HX + 4 * tx;
+    const int toff = ty * C::TX + 4 * tx;
 
     for (;;) {
         const int item = fast::wq_next(P.wq, &s_item);
@@ -239,33 +284,36 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
             const int s = j % C::NSV;
             const uint32_t bar = bar0 + 8 * s;
             fast::mbar_expect_tx(bar, 4u * C::BX * C::BY);
-            fast::tma_load_3d(smem_u32(ring + s * C::PPLANE), &tm_p, L.L + x0 - C::HX,
+            fast::tma_load_3d(smem_u32(ring + s * C::PPLANE), &M.p, L.L + x0 - C::HX,
                               y0 - R + L.r, zb - R + 1 + j + L.r, bar);
         };
-        if (tid == 0)
+        const unsigned qbase = qn;
+        auto issue_q = [&](int o) {
+            const int st = (qbase + o) % C::NQV;
+            const uint32_t bar = barQ + 8 * st;
+            float* dst = qring + st * 4 * C::TILE;
+            const int zz = zb + o + L.r, xx = L.L + x0, yy = y0 + L.r;
+            fast::mbar_expect_tx(bar, 4u * 4 * C::TX * C::TY);
+            fast::tma_load_3d(smem_u32(dst), &M.ir, xx, yy, zz, bar);
+            fast::tma_load_3d(smem_u32(dst + C::TILE), &M.vx, xx, yy, zz, bar);
+            fast::tma_load_3d(smem_u32(dst + 2 * C::TILE), &M.vy, xx, yy, zz, bar);
+            fast::tma_load_3d(smem_u32(dst + 3 * C::TILE), &M.vz, xx, yy, zz, bar);
+        };
+        if (tid == 0) {
             for (int j = 0; j < min(C::NSV, nring); ++j) issue(j);
+            for (int o = 0; o < min(C::NQV, nout); ++o) issue_q(o);
+        }
         PointSet S;
         point_set<R>(S, P, x0, y0, tx, ty, zb);
         const long long o0 = L.off(S.xg, S.y, zb);
-        // point-wise streams, one plane ahead
-        float4 cir, cv[3], nir = make_float4(0.f, 0.f, 0.f, 0.f), nv[3];
-        if (S.any) {
-            cir = ld4z(P.ir + o0, S);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) cv[a] = ld4z(P.v[a] + o0, S);
-        }
         for (int j = 0; j < 2 * R - 1; ++j) {
             fast::mbar_wait(bar0 + 8 * (j % C::NSV), (ph >> (j % C::NSV)) & 1u);
             ph ^= 1u << (j % C::NSV);
         }
         for (int o = 0; o < nout; ++o) {
             const int k = zb + o;
-            const long long oo = o0 + (long long)o * L.plane;
-            if (S.any && o + 1 < nout) {
-                nir = ld4z(P.ir + oo + L.plane, S);
-#pragma unroll
-                for (int a = 0; a < 3; ++a) nv[a] = ld4z(P.v[a] + oo + L.plane, S);
-            }
+            PsiState ps;
+            psi_load(ps, P, S, o, k);
             const int jn = o + 2 * R - 1;  // newest plane of the window
             fast::mbar_wait(bar0 + 8 * (jn % C::NSV), (ph >> (jn % C::NSV)) & 1u);
             ph ^= 1u << (jn % C::NSV);
@@ -309,52 +357,65 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
                 for (int e = 0; e < 4; ++e)
                     d[2][e] = fa(d[2][e], fm(P.w[2][m - 1], fs(comp(u, e), comp(dn, e))));
             }
+            const int st = qn % C::NQV;
+            fast::mbar_wait(barQ + 8 * st, (phQ >> st) & 1u);
+            phQ ^= 1u << st;
+            ++qn;
             if (S.any) {
-                cpml_plane(d, P, S, o, k);
-                float out[3][4];
+                psi_apply(d, ps, P, S, o, k);
+                const float* Q = qring + st * 4 * C::TILE + toff;
+                const float4 ir = lds4(Q);
+                const long long oo = o0 + (long long)o * L.plane;
 #pragma unroll
-                for (int a = 0; a < 3; ++a)
+                for (int a = 0; a < 3; ++a) {
+                    const float4 v = lds4(Q + (a + 1) * C::TILE);
+                    float out[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) out[a][e] = fa(comp(cv[a], e), fm(comp(cir, e), d[a][e]));
-#pragma unroll
-                for (int a = 0; a < 3; ++a) st4v(P.v[a] + oo, out[a], S);
-                cir = nir;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) cv[a] = nv[a];
+                    for (int e = 0; e < 4; ++e) out[e] = fa(comp(v, e), fm(comp(ir, e), d[a][e]));
+                    st4v(P.v[a] + oo, out, S);
+                }
             }
-            __syncthreads();  // plane o (the window's oldest) is free
-            if (tid == 0 && o + C::NSV < nring) issue(o + C::NSV);
+            __syncthreads();  // plane o (the window's oldest) and stage o are free
+            if (tid == 0) {
+                if (o + C::NSV < nring) issue(o + C::NSV);
+                if (o + C::NQV < nout) issue_q(o + C::NQV);
+            }
         }
-        // planes issued but not consumed as "newest": none (the loop waited on
-        // every plane up to nring - 1)
     }
     fast::wq_done(P.wq);
 }
 
 // ----------------------------------------------------------------- pressure
+// maps: vx (BX x TY, x halo), vy (TX x BY, y halo), vz, dtb, p (TX x TY tiles)
+struct VdpMaps {
+    CUtensorMap vx, vy, vz, dtb, p;
+};
+
 template <int R>
 __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
-    k_vdp(const __grid_constant__ CUtensorMap tm_vx, const __grid_constant__ CUtensorMap tm_vy,
-          const __grid_constant__ CUtensorMap tm_vz, const VdFastParams P) {
+    k_vdp(const __grid_constant__ VdpMaps M, const VdFastParams P) {
     using C = VdCfg<R>;
+    constexpr int QST = C::VXB + C::VYB + 2 * C::TILE;  // floats per stage
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
     float* qring = ring + C::NSP * C::TILE;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(qring + C::NQP * (C::VXB + C::VYB));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(qring + C::NQP * QST);
     const uint32_t barZ = smem_u32(bars), barQ = smem_u32(bars + C::NSP);
     const int tid = threadIdx.x;
     const int tx = tid % C::TXT, ty = tid / C::TXT;
     const Layout L = P.lay;
     if (tid == 0) {
-        fast::prefetch_tmap(&tm_vx);
-        fast::prefetch_tmap(&tm_vy);
-        fast::prefetch_tmap(&tm_vz);
+        fast::prefetch_tmap(&M.vx);
+        fast::prefetch_tmap(&M.vy);
+        fast::prefetch_tmap(&M.vz);
+        fast::prefetch_tmap(&M.dtb);
+        fast::prefetch_tmap(&M.p);
         for (int s = 0; s < C::NSP + C::NQP; ++s) fast::mbar_init(barZ + 8 * s, 1);
         fast::fence_barrier_init();
     }
     __syncthreads();
     uint32_t phZ = 0, phQ = 0;
-    unsigned qn = 0;  // stages consumed (all threads), == stages issued - NQP in flight
+    unsigned qn = 0;
     __shared__ int s_item;
     const int toff = ty * C::TX + 4 * tx;
     const int xoff = ty * C::BX + C::HX + 4 * tx;  // in a vx box
@@ -371,18 +432,22 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
             const int s = j % C::NSP;
             const uint32_t bar = barZ + 8 * s;
             fast::mbar_expect_tx(bar, 4u * C::TX * C::TY);
-            fast::tma_load_3d(smem_u32(ring + s * C::TILE), &tm_vz, L.L + x0, y0 + L.r,
+            fast::tma_load_3d(smem_u32(ring + s * C::TILE), &M.vz, L.L + x0, y0 + L.r,
                               zb - R + j + L.r, bar);
         };
         const unsigned qbase = qn;
         auto issue_q = [&](int o) {
             const int st = (qbase + o) % C::NQP;
             const uint32_t bar = barQ + 8 * st;
-            float* dst = qring + st * (C::VXB + C::VYB);
-            fast::mbar_expect_tx(bar, 4u * (C::BX * C::TY + C::TX * C::BY));
-            fast::tma_load_3d(smem_u32(dst), &tm_vx, L.L + x0 - C::HX, y0 + L.r, zb + o + L.r, bar);
-            fast::tma_load_3d(smem_u32(dst + C::VXB), &tm_vy, L.L + x0, y0 - R + L.r,
-                              zb + o + L.r, bar);
+            float* dst = qring + st * QST;
+            const int zz = zb + o + L.r;
+            fast::mbar_expect_tx(bar, 4u * (C::BX * C::TY + C::TX * C::BY + 2 * C::TX * C::TY));
+            fast::tma_load_3d(smem_u32(dst), &M.vx, L.L + x0 - C::HX, y0 + L.r, zz, bar);
+            fast::tma_load_3d(smem_u32(dst + C::VXB), &M.vy, L.L + x0, y0 - R + L.r, zz, bar);
+            fast::tma_load_3d(smem_u32(dst + C::VXB + C::VYB), &M.dtb, L.L + x0, y0 + L.r, zz,
+                              bar);
+            fast::tma_load_3d(smem_u32(dst + C::VXB + C::VYB + C::TILE), &M.p, L.L + x0,
+                              y0 + L.r, zz, bar);
         };
         if (tid == 0) {
             for (int j = 0; j < min(C::NSP, nring); ++j) issue_z(j);
@@ -391,29 +456,22 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
         PointSet S;
         point_set<R>(S, P, x0, y0, tx, ty, zb);
         const long long o0 = L.off(S.xg, S.y, zb);
-        float4 cdt, cp, ndt = make_float4(0.f, 0.f, 0.f, 0.f), np_ = ndt;
-        if (S.any) {
-            cdt = ld4z(P.dtb + o0, S);
-            cp = ld4z(P.p + o0, S);
-        }
         for (int j = 0; j < 2 * R - 1; ++j) {
             fast::mbar_wait(barZ + 8 * (j % C::NSP), (phZ >> (j % C::NSP)) & 1u);
             phZ ^= 1u << (j % C::NSP);
         }
         for (int o = 0; o < nout; ++o) {
             const int k = zb + o;
-            const long long oo = o0 + (long long)o * L.plane;
-            if (S.any && o + 1 < nout) {
-                ndt = ld4z(P.dtb + oo + L.plane, S);
-                np_ = ld4z(P.p + oo + L.plane, S);
-            }
+            PsiState ps;
+            psi_load(ps, P, S, o, k);
             const int jn = o + 2 * R - 1;
             fast::mbar_wait(barZ + 8 * (jn % C::NSP), (phZ >> (jn % C::NSP)) & 1u);
             phZ ^= 1u << (jn % C::NSP);
             const int st = qn % C::NQP;
             fast::mbar_wait(barQ + 8 * st, (phQ >> st) & 1u);
             phQ ^= 1u << st;
-            const float* Q = qring + st * (C::VXB + C::VYB);
+            ++qn;
+            const float* Q = qring + st * QST;
             float d[3][4];
             // x: t += c_m (vx[x+m-1] - vx[x-m])
             {
@@ -453,16 +511,15 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, 2)
                 for (int e = 0; e < 4; ++e)
                     d[2][e] = fa(d[2][e], fm(P.w[2][m - 1], fs(comp(u, e), comp(dn, e))));
             }
-            ++qn;
             if (S.any) {
-                cpml_plane(d, P, S, o, k);
+                psi_apply(d, ps, P, S, o, k);
+                const float4 dt = lds4(Q + C::VXB + C::VYB + toff);
+                const float4 pc = lds4(Q + C::VXB + C::VYB + C::TILE + toff);
                 float out[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    out[e] = fa(comp(cp, e), fm(comp(cdt, e), fa(fa(d[0][e], d[1][e]), d[2][e])));
-                st4v(P.p + oo, out, S);
-                cdt = ndt;
-                cp = np_;
+                    out[e] = fa(comp(pc, e), fm(comp(dt, e), fa(fa(d[0][e], d[1][e]), d[2][e])));
+                st4v(P.p + o0 + (long long)o * L.plane, out, S);
             }
             __syncthreads();  // vz plane o and stage o are free
             if (tid == 0) {
