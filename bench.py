@@ -3,6 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--grid 240] [--mode fast|strict] [--radius 4]
+                    [--propagator acoustic_iso_cd|acoustic_iso]
 
 A "step" is one time step of the propagator over the whole grid (the
 reference's eng.step(), driver.cpp:104-106).  Workload at N=1: BASELINE.json
@@ -59,6 +60,9 @@ def parse():
     ap.add_argument("--radius", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=None)
+    ap.add_argument("--propagator", default="acoustic_iso_cd",
+                    choices=["acoustic_iso_cd", "acoustic_iso"],
+                    help="acoustic_iso: the variable-density engine (SURVEY 8(f) row 4)")
     return ap.parse_args()
 
 
@@ -121,12 +125,20 @@ def ncu_traffic(workload, kernel):
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_reference_run(n, nsteps, nthreads):
+def cpu_reference_run(n, nsteps, nthreads, propagator="acoustic_iso_cd"):
     from oracle.oracle import Oracle, available, nproc
     kind = "reference" if available("reference") else "port"
     o = Oracle(kind)
     vp, vmin, vmax = o.layered_model(n)
-    if kind == "reference":
+    if propagator == "acoustic_iso":
+        rho = np.full_like(vp, 1000.0)  # default_layered_model's rho (model.cpp:63-77)
+        if kind == "reference":
+            out = o.run_vd(n, vp, rho, nsteps=nsteps, nthreads=nthreads)
+            threads = nthreads
+        else:
+            out = o.run_vd(n, vp, rho, nsteps=nsteps, vmax=vmax)
+            threads = 1
+    elif kind == "reference":
         out = o.run(n, vp, nsteps=nsteps, nthreads=nthreads)
         threads = nthreads
     else:
@@ -303,6 +315,146 @@ def run_ours(args):
     return 0
 
 
+VD_METRIC = "Gpoints/s (grid-point updates/sec) acoustic_iso 8th-order"
+
+
+def vd_kernel_bytes(n, nd):
+    """Compulsory bytes per launch of k_vdv / k_vdp (vd_engine.cu): velocity
+    reads p, dt/rho, v and writes v (32 B/pt), pressure reads v, dt*bulk, p and
+    writes p (24 B/pt); plus 8 B (psi r+w) per damping-layer point and axis."""
+    N = n[0] * n[1] * n[2]
+    lay = sum(2 * nd[a] * N // n[a] for a in range(3))
+    return {"velocity": 32 * N + 8 * lay, "pressure": 24 * N + 8 * lay}
+
+
+def run_vd(args):
+    """The acoustic_iso leg: same contract as run_ours (N = 1)."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+    import paper_2007_06048_b200 as mm
+    from paper_2007_06048_b200 import _lib
+
+    edge = args.grid or 240
+    n = (edge, edge, edge)
+    nd = (27, 27, 27)
+    torch.cuda.set_device(local)
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0), args.radius)
+    model = mm.default_layered_model(grid)
+    dt = mm.cfl_dt(model, grid, 0.8)
+    total = args.warmup + args.steps
+    w = mm.integrate_wavelet(mm.ricker(25.0, dt, total)).samples
+    src = tuple(x // 2 for x in n)
+    opts = mm.EngineOptions(ndamping=nd, taper=True)
+    geo = mm.default_receivers(grid, nd)
+    nrec = geo.nreceivers()
+    eng = mm.AcousticVdEngine(grid, model, opts, dt, device=local)
+    eng.set_receivers(geo.receivers, total)
+    ext = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
+    t_ramp = time.perf_counter()
+    while time.perf_counter() - t_ramp < 0.3:
+        eng.run(w[:min(total, 50)], src, record=False)
+        eng.synchronize()
+    del eng
+    eng = mm.AcousticVdEngine(grid, model, opts, dt, device=local)
+    eng.set_receivers(geo.receivers, total)
+    ext = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
+    eng.run(w[:args.warmup], src, record=True, first_sample=0)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.kernel_launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(ext)
+    eng.run(w[args.warmup:total], src, record=True, first_sample=args.warmup)
+    t1.record(ext)
+    t1.synchronize()
+    launches = _lib.kernel_launch_count() - launches0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    pts = float(n[0]) * n[1] * n[2]
+    value = pts * args.steps / (ms * 1e-3) / 1e9
+    # per-kernel durations (CUDA events on the engine stream)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for s in range(args.steps):
+        ev[s][0].record(ext)
+        eng.update_velocity()
+        ev[s][1].record(ext)
+        eng.update_pressure()
+        ev[s][2].record(ext)
+        eng.inject_source(float(w[s % total]), src)
+    torch.cuda.synchronize()
+    kms = {k: statistics.mean(e[i].elapsed_time(e[i + 1]) for e in ev)
+           for i, k in enumerate(("velocity", "pressure"))}
+    # e2e through the public API with host buffers
+    eng2 = mm.AcousticVdEngine(grid, model, opts, dt, device=local)
+    eng2.set_receivers(geo.receivers, total)
+    host_out = torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
+    for s in range(args.warmup):
+        eng2.step(float(w[s]), src)
+        eng2.record(s)
+    eng2.synchronize()
+    ext2 = torch.cuda.ExternalStream(eng2.stream_handle(), device=local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    e0.record(ext2)
+    for s in range(args.warmup, total):
+        eng2.step(float(w[s]), src)
+        eng2.record(s)
+        eng2.copy_trace_step(s, host_out[s - args.warmup], asynchronous=True)
+    e1.record(ext2)
+    eng2.synchronize()
+    wall = time.perf_counter() - wall0
+    e2e_ms = max(e0.elapsed_time(e1), wall * 1e3)
+    e2e = pts * args.steps / (e2e_ms * 1e-3) / 1e9
+
+    peak, peak_src = measured_peak()
+    kb = vd_kernel_bytes(n, nd)
+    dominant = max(kms, key=kms.get)
+    achieved = kb[dominant] / (kms[dominant] * 1e-3) / 1e9
+    ref_model = 40 * pts  # the reference's fused cost model (bench.cpp:97)
+    step_gbs = ref_model * args.steps / (ms * 1e-3) / 1e9
+    line = {
+        "metric": VD_METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (default two-layer model: vp 1500/4500, rho 1000; integrated Ricker)",
+        "config": {"workload": f"acoustic_iso r={args.radius} {edge}^3 grid, nd=27 CPML, taper, "
+                               f"{nrec} surface receivers", "grid": list(n),
+                   "radius": args.radius, "ndamping": list(nd),
+                   "l2": "working set (p, v, dt/rho, dt*bulk, CPML) > 126 MB L2; no flush"},
+        "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": 4 * nrec},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": dominant, "algorithmic_bytes_per_launch": kb[dominant],
+                     "kernel_ms": round(kms[dominant], 4), "peak_source": peak_src},
+        "kernels": {k: {"ms": round(kms[k], 4), "algorithmic_bytes": kb[k],
+                        "achieved_gbs": round(kb[k] / (kms[k] * 1e-3) / 1e9, 1)} for k in kms},
+        "step_roofline": {"bytes_per_step_model": ref_model,
+                          "model": "reference cost model 40 B/pt (bench.cpp:97)",
+                          "achieved_gbs": round(step_gbs, 1), "frac": round(step_gbs / peak, 4),
+                          "roofline_gpts": round(peak / 40, 1)},
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        ns = cpu_sample_steps(n, args.cpu_sample_steps)
+        from oracle.oracle import nproc
+        gpts, kind, threads, secs = cpu_reference_run(n, ns, nproc(), "acoustic_iso")
+        line["cpu_baseline"] = {"value": round(gpts, 5), "unit": UNIT, "cores": threads,
+                                "kind": kind,
+                                "sample": f"{edge}^3 x {ns} steps from t=0 ({secs:.1f} s), "
+                                          "run(AcousticIso) Target::Parallel"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -312,14 +464,15 @@ def run_reference(args):
     cores = nproc()
     ns = max(1, min(args.steps, cpu_sample_steps(n, args.cpu_sample_steps)))
     # warm-up: one short run (page in, thread start-up)
-    cpu_reference_run(n, max(1, min(args.warmup, 2)), cores)
-    gpts, kind, threads, secs = cpu_reference_run(n, ns, cores)
+    cpu_reference_run(n, max(1, min(args.warmup, 2)), cores, args.propagator)
+    gpts, kind, threads, secs = cpu_reference_run(n, ns, cores, args.propagator)
+    vd = args.propagator == "acoustic_iso"
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(gpts, 5), "unit": UNIT,
+        "impl": "reference", "metric": VD_METRIC if vd else METRIC, "value": round(gpts, 5), "unit": UNIT,
         "n_gpus": world, "steps": ns, "warmup": args.warmup,
         "ms_per_step": secs * 1e3 / ns, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (default two-layer model)",
-        "config": {"workload": f"acoustic_iso_cd r=4 {n[0]}x{n[1]}x{n[2]} grid, nd=27 CPML, "
+        "config": {"workload": f"{args.propagator} r=4 {n[0]}x{n[1]}x{n[2]} grid, nd=27 CPML, "
                                f"taper (bounded sample: {ns} steps from t=0)", "grid": list(n)},
         "cpu_baseline": {"value": round(gpts, 5), "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{n[0]}x{n[1]}x{n[2]} x {ns} steps, run() Target::Parallel"},
@@ -334,6 +487,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.propagator == "acoustic_iso":
+        return run_vd(args)
     return run_ours(args)
 
 

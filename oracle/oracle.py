@@ -256,6 +256,22 @@ class Oracle:
                                             C.byref(vmin), C.byref(vmax)))
         return tuple(n), tuple(d), vp, vmin.value, vmax.value
 
+    def save_model_rho(self, vp, rho, n, d, radius, manifest):
+        """save_model (model.cpp:157-184) of a model with a density volume."""
+        self._ref_only()
+        v = np.ascontiguousarray(vp, dtype=np.float32)
+        r = np.ascontiguousarray(rho, dtype=np.float32)
+        self._check(self.lib.ref_save_model_rho(_i3(*n), _d3(*d), C.c_int(radius), _f32(v),
+                                                _f32(r), str(manifest).encode()))
+
+    def load_model_rho(self, manifest, n, radius=4):
+        """rho of load_model (model.cpp:122-155), or None."""
+        self._ref_only()
+        rho = np.zeros(ghosted_shape(tuple(n), radius), np.float32)
+        has = C.c_int()
+        self._check(self.lib.ref_load_model_rho(str(manifest).encode(), _f32(rho), C.byref(has)))
+        return rho if has.value else None
+
     def render_report(self, *, ngrid, dgrid, nsteps, fmax, cfl, radius, ndamping, ntaper,
                       source_loc, receiver_increment, source_increment, nshots, time_rec,
                       nthreads, vmin, vmax, kernel_s, modeling_s):

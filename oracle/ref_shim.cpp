@@ -147,6 +147,9 @@ int ref_run(const int n[3], const double d[3], int radius, int nsteps, double fm
     }
 }
 
+static EarthModel make_vd_model(const int n[3], const double d[3], int radius, const float* vp,
+                                const float* rho);
+
 struct ref_engine {
     AcousticCdEngine<float>* eng;
     int nthreads;
@@ -280,6 +283,30 @@ int ref_load_model(const char* manifest, int n[3], double d[3], float* vp, float
         if (vp) std::memcpy(vp, m.vp.data.data(), sizeof(float) * m.vp.data.size());
         *vmin = m.vmin;
         *vmax = m.vmax;
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+// save_model of a model with a density volume (rho.f32 next to vp.f32)
+int ref_save_model_rho(const int n[3], const double d[3], int radius, const float* vp,
+                       const float* rho, const char* manifest) {
+    try {
+        const EarthModel m = make_vd_model(n, d, radius, vp, rho);
+        save_model(m, manifest);
+        return 0;
+    } catch (...) {
+        return catch_all();
+    }
+}
+
+// rho of a loaded manifest (ghosted, radius 4); *has = 0 when it lists none
+int ref_load_model_rho(const char* manifest, float* rho, int* has) {
+    try {
+        const EarthModel m = load_model(manifest);
+        *has = m.rho.has_value() ? 1 : 0;
+        if (m.rho && rho) std::memcpy(rho, m.rho->data.data(), sizeof(float) * m.rho->data.size());
         return 0;
     } catch (...) {
         return catch_all();

@@ -1,9 +1,9 @@
 """`python -m paper_2007_06048_b200 model ...` -- the reference's `minimod model`
 front end (ref: tools/cli.cpp:60-101, 256-272) on the B200 engine.
 
-Same flags and output for the acoustic_iso_cd path: the parameter block, the
-run, the timing lines, and the shot record (raw f32 + JSON sidecar) when
---output is given.  Exit codes as the reference: 2 for configuration errors,
+Same flags and output for the acoustic_iso_cd path (and acoustic_iso, the
+variable-density engine): the parameter block, the run, the timing lines, and
+the shot record (raw f32 + JSON sidecar) when --output is given.  Exit codes as the reference: 2 for configuration errors,
 3 for anything else.  `--kernels fast|strict` selects the kernel family (both
 bit-identical to the CPU reference); `--device` the GPU.
 """
@@ -50,8 +50,9 @@ def parse(argv):
         raise ConfigError("cannot parse the command line") from None
     if unknown:
         raise ConfigError(f"unknown arguments: {' '.join(unknown)}")
-    if a.propagator != "acoustic_iso_cd":
-        raise ConfigError(f"--propagator {a.propagator}: this build serves acoustic_iso_cd only")
+    if a.propagator not in ("acoustic_iso_cd", "acoustic_iso"):
+        raise ConfigError(f"--propagator {a.propagator}: this build serves acoustic_iso_cd and "
+                          "acoustic_iso")
     a.ngrid = _tuple("--ngrid", a.ngrid, int)
     a.dgrid = _tuple("--dgrid", a.dgrid, float)
     if a.nsteps < 1:
@@ -77,8 +78,8 @@ def main(argv=None, out=sys.stdout, err=sys.stderr) -> int:
         return 2
     try:
         from . import driver, numerics, shotio
-        cfg = driver.SimConfig(ngrid=a.ngrid, dgrid=a.dgrid, nsteps=a.nsteps, fmax=a.fmax,
-                               free_surface=a.free_surface)
+        cfg = driver.SimConfig(propagator=a.propagator, ngrid=a.ngrid, dgrid=a.dgrid,
+                               nsteps=a.nsteps, fmax=a.fmax, free_surface=a.free_surface)
         grid = numerics.make_grid(cfg.ngrid, cfg.dgrid, cfg.stencil_radius)
         if a.model_manifest:
             model = shotio.load_model(a.model_manifest, cfg.stencil_radius)

@@ -223,11 +223,23 @@ struct mm_cd_engine {
             if (free_surface && goff[2] == 0) launch_free_surface(p[in].ptr, lay, stream);
             rotate();
             ++steps;
+            debug_sync("fast");
             return;
         }
         pass1();
         update(0, 0, lay.n[2]);
         finish_step(amp, src, amp_dev, step_dev);
+        debug_sync("strict");
+    }
+    // MM_DEBUG_SYNC=all|fast|strict: synchronize after every step and name the engine whose
+    // step faulted (diagnostics only)
+    void debug_sync(const char* what) {
+        static const char* sel = std::getenv("MM_DEBUG_SYNC");
+        if (!sel || !(std::strcmp(sel, "all") == 0 || std::strcmp(sel, what) == 0)) return;
+        const cudaError_t e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess)
+            raise(ST_CUDA, std::string("fault in ") + what + " step " + std::to_string(steps) +
+                               ": " + cudaGetErrorString(e));
     }
 
     void to_host(const float* dev, float* host) {

@@ -343,8 +343,10 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
         const float aya = __ldg(P.ta[1] + yc), ayb = __ldg(P.tb[1] + yc),
                     ayk = __ldg(P.tik[1] + yc);
         // zeta_y: the y run holding this row (a tile may meet both runs)
+        // (only where the tile's stage carries that run's zeta_y: Z-slab tiles
+        // never do, although rows past their box may fall in a y run)
         const int zyside = in_run(P.run[1][0], y) ? 0 : in_run(P.run[1][1], y) ? 1 : -1;
-        const bool y_in_zy = zyside >= 0;
+        const bool y_in_zy = zyside == 0 ? T.fzy0 : zyside == 1 ? T.fzy1 : false;
         // streams: element (xg, y, z) at base + (z - zb) * step
         const long long foff = L.off(xg, y, T.zb);
         float* pn_p = P.pn + foff;
@@ -434,8 +436,8 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                     const int qsz = T.qsize + (zr >= 0 ? C::TILE : 0) + (zex >= 0 ? C::TILE : 0);
                     if (qo + qsz > C::QB) qo = 0;  // a stage never wraps (q_alloc)
                     const float* Q = qring + qo;
-                    qo += qsz;
                     mbar_wait(fullQ + 8 * st, (nq / C::NQD) & 1);
+                    qo += qsz;
                     pp = lds4(Q + toff);
                     cv = lds4(Q + C::TILE + toff);
                     if (fx) zx = lds4(Q + T.o_zx + toff);

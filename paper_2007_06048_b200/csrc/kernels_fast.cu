@@ -334,16 +334,33 @@ public:
             launch_inner(p, 0, lay_.n[2], imode, side_);
             MM_CUDA(cudaEventRecord(join_, side_));
         }
+        dbg(s, "inner(side)", ov ? side_ : nullptr);
         launch_pass1(p, 0, lay_.n[2], s);
+        dbg(s, "pass1", p1_side_);
         if (fc)
             launch_boundary(p, 0, lay_.n[2], s);
         else
             strict_update(p, 2, 0, lay_.n[2], s);
+        dbg(s, "boundary", nullptr);
         if (ov)
             MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
         else
             launch_inner(p, 0, lay_.n[2], imode, s);
+        dbg(s, "inner", nullptr);
         if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
+    }
+    // MM_DEBUG_SYNC=kernels: synchronize after each kernel of the step and name
+    // the one that faulted (diagnostics only)
+    void dbg(cudaStream_t s, const char* what, cudaStream_t s2) {
+        static const bool on = [] {
+            const char* e = std::getenv("MM_DEBUG_SYNC");
+            return e && std::strcmp(e, "kernels") == 0;
+        }();
+        if (!on) return;
+        cudaError_t e = s2 ? cudaStreamSynchronize(s2) : cudaSuccess;
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess)
+            raise(ST_CUDA, std::string("fault after ") + what + ": " + cudaGetErrorString(e));
     }
 
 private:
@@ -651,10 +668,16 @@ private:
             bp_.pn = p.pn;
             bp_.segs = w.segs.ptr;
             bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
+            // MM_BND_CTAS (diagnostics): cap the CTA count (more items per CTA)
+            static const int cap = [] {
+                const char* e = std::getenv("MM_BND_CTAS");
+                return e ? std::max(1, std::atoi(e)) : 1 << 30;
+            }();
+            const int ctas = std::min(w.ctas, cap);
             if (order_ == 2)
-                launch_pdl(k_bnd<R, 2>, w.ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
+                launch_pdl(k_bnd<R, 2>, ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
             else
-                launch_pdl(k_bnd<R, 1>, w.ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
+                launch_pdl(k_bnd<R, 1>, ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
             note_launches(1);
             MM_CUDA(cudaGetLastError());
         }

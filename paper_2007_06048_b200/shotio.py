@@ -116,21 +116,40 @@ def load_record(path) -> ShotRecord:
 
 # ------------------------------------------------------------------ models
 def save_model(model: EarthModel, manifest) -> None:
-    """ref: model.cpp:160-190 (vp only: the acoustic_iso_cd path)."""
+    """ref: model.cpp:157-184 (vp, and rho when the model has one)."""
     manifest = Path(manifest)
     if not str(manifest):
         raise ConfigError("empty model manifest path")
     g = model.grid
-    vol = np.ascontiguousarray(g.inner(np.asarray(model.vp, dtype=np.float32)), dtype="<f4")
-    vp_path = manifest.parent / "vp.f32"
-    os.replace(_write_atomic(vp_path, vol.tobytes()), vp_path)
+    comps = {}
+    for name, field in (("vp", model.vp), ("rho", model.rho)):
+        if field is None:
+            continue
+        vol = np.ascontiguousarray(g.inner(np.asarray(field, dtype=np.float32)), dtype="<f4")
+        path = manifest.parent / f"{name}.f32"
+        os.replace(_write_atomic(path, vol.tobytes()), path)
+        comps[name] = f"{name}.f32"
     man = {"n": [int(x) for x in g.n], "d": [float(x) for x in g.d],
-           "components": {"vp": "vp.f32"}, "dtype": "f32le", "order": "z-fastest"}
+           "components": comps, "dtype": "f32le", "order": "z-fastest"}
     os.replace(_write_atomic(manifest, (_dump(man) + "\n").encode()), manifest)
 
 
+def _read_volume(path: Path, grid, count: int) -> np.ndarray:
+    try:
+        nbytes = path.stat().st_size
+    except OSError as e:
+        raise ConfigError(f"cannot open volume file: {path}") from e
+    if nbytes != 4 * count:
+        raise ConfigError(f"size mismatch for {path}: manifest implies {4 * count} bytes, "
+                          f"file has {nbytes}")
+    f = grid.field()
+    grid.inner(f)[...] = np.fromfile(path, dtype="<f4").reshape(grid.n)
+    return f
+
+
 def load_model(manifest, radius: int = 4) -> EarthModel:
-    """ref: model.cpp:64-99 -- manifest + f32 volume -> validated, ghosted vp."""
+    """ref: model.cpp:122-155 -- manifest + f32 volumes -> validated, ghosted
+    vp (and rho when the manifest lists one; vs is elastic-only and ignored)."""
     manifest = Path(manifest)
     if not str(manifest):
         raise ConfigError("empty model manifest path")
@@ -147,18 +166,13 @@ def load_model(manifest, radius: int = 4) -> EarthModel:
     try:
         n = tuple(int(x) for x in j["n"])
         d = tuple(float(x) for x in j["d"])
-        vp_file = manifest.parent / j["components"]["vp"]
+        comps = j["components"]
+        vp_file = manifest.parent / comps["vp"]
+        rho_file = manifest.parent / comps["rho"] if "rho" in comps else None
     except (KeyError, TypeError) as e:
         raise ConfigError(f"malformed model manifest {manifest}: missing {e}") from e
     grid = make_grid(n, d, radius)
     count = n[0] * n[1] * n[2]
-    try:
-        nbytes = vp_file.stat().st_size
-    except OSError as e:
-        raise ConfigError(f"cannot open volume file: {vp_file}") from e
-    if nbytes != 4 * count:
-        raise ConfigError(f"size mismatch for {vp_file}: manifest implies {4 * count} bytes, "
-                          f"file has {nbytes}")
-    vp = grid.field()
-    grid.inner(vp)[...] = np.fromfile(vp_file, dtype="<f4").reshape(n)
-    return validate_model(EarthModel(grid, vp))
+    vp = _read_volume(vp_file, grid, count)
+    rho = _read_volume(rho_file, grid, count) if rho_file is not None else None
+    return validate_model(EarthModel(grid, vp, rho=rho))

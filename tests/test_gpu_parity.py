@@ -5,10 +5,12 @@ Bar (BASELINE.json north_star): MM_MODE_STRICT is bit-identical to the CPU
 reference; MM_MODE_FAST (FMA-contracted, reassociated stencil) keeps the final
 wavefield within relative L2 <= 1e-5 of it (max-abs reported in the message).
 """
+import os
+
 import numpy as np
 import pytest
 
-from conftest import load_golden
+from conftest import ROOT, load_golden
 
 pytestmark = pytest.mark.gpu
 
@@ -321,3 +323,35 @@ def test_instability_is_reported_with_step(mm):
     with pytest.raises(mm.InstabilityError) as ei:
         e.run(amps, (12, 12, 12))
     assert 1 <= ei.value.step <= 400
+
+
+@pytest.mark.parametrize("ctas", ["16", "3"])
+def test_fast_boundary_few_ctas_regression(ctas, tmp_path):
+    """k_bnd with few CTAs (MM_BND_CTAS, read once per process): each CTA
+    pulls long mixed sequences of X/Y/Z-slab items through its stage ring.
+    Regression for a Z-slab tile whose rows past its box fall in a y damping
+    run: it read a zeta_y stage region its stage does not carry (out of the
+    ring's shared memory when the stage sat at the ring's end)."""
+    import subprocess
+    import sys
+    script = tmp_path / "few_ctas.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import paper_2007_06048_b200 as mm\n"
+        "n, nd, src = (61, 47, 53), (9, 7, 11), (30, 23, 40)\n"
+        "g = mm.make_grid(n, (20.0, 15.0, 10.0), 4)\n"
+        "m = mm.random_model(g, seed=11)\n"
+        "w = mm.ricker(25.0, 1e-3, 60).samples\n"
+        "o = mm.EngineOptions(ndamping=nd, taper=True, free_surface=True)\n"
+        "e = {md: mm.AcousticCdEngine(g, (0, 0, 0), n, m.vp, o, 1e-3, m.vmax, mode=md)\n"
+        "     for md in ('fast', 'strict')}\n"
+        "for s in range(60):\n"
+        "    for x in e.values():\n"
+        "        x.step(float(w[s]), src)\n"
+        "assert np.array_equal(e['fast'].pressure(), e['strict'].pressure())\n"
+        "print('ok')\n")
+    env = dict(os.environ, MM_BND_CTAS=ctas)
+    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

@@ -166,3 +166,41 @@ def test_vd_large_grid_against_oracle(mm, oracle_port):
             o.step(float(w[s]) * 1e6, (30, 60, 100))
         assert np.array_equal(e.pressure(), o.pressure())
         assert np.array_equal(e.velocity(2), o.velocity(2))
+
+
+def test_vd_cli_model_run(mm, tmp_path, oracle_ref):
+    """`minimod model --propagator acoustic_iso` (tools/cli.cpp:256-272)."""
+    import io
+    from paper_2007_06048_b200.__main__ import main
+    out, err = io.StringIO(), io.StringIO()
+    n = (60, 56, 64)  # default ndamping 27 needs n > 54
+    rc = main(["model", "--propagator", "acoustic_iso", "--ngrid", ",".join(map(str, n)),
+               "--nsteps", "30", "--output", str(tmp_path / "shot.bin")], out, err)
+    assert rc == 0, err.getvalue()
+    assert "Time Kernel" in out.getvalue()
+    rec = mm.load_record(tmp_path / "shot.bin")
+    model = mm.default_layered_model(mm.make_grid(n, (20.0, 20.0, 20.0)))
+    ref = oracle_ref.run_vd(n, model.vp, model.rho, nsteps=30)
+    assert np.array_equal(rec.traces, ref["traces"])
+
+
+def test_vd_kernel_families_agree(mm, monkeypatch):
+    """The TMA kernels (default) and the plain one-thread-per-point restatement
+    (MM_VD_SIMPLE=1, read at engine creation) are bit-identical."""
+    n, r = (70, 66, 75), 4
+    g, m = _model(mm, n, r, seed=11)
+    opts = mm.EngineOptions(ndamping=(9, 10, 11), free_surface=True, taper=True)
+    dt = 1e-3
+    w = mm.integrate_wavelet(mm.ricker(25.0, dt, 40)).samples
+    fast = mm.AcousticVdEngine(g, m, opts, dt)
+    monkeypatch.setenv("MM_VD_SIMPLE", "1")
+    plain = mm.AcousticVdEngine(g, m, opts, dt)
+    monkeypatch.delenv("MM_VD_SIMPLE")
+    for s in range(40):
+        fast.step(float(w[s]) * 1e6, (20, 30, 40))
+        plain.step(float(w[s]) * 1e6, (20, 30, 40))
+    assert np.array_equal(fast.pressure(), plain.pressure())
+    for ax in range(3):
+        assert np.array_equal(fast.velocity(ax), plain.velocity(ax))
+    fast.close()
+    plain.close()

@@ -134,3 +134,27 @@ def test_cli_help():
     out = io.StringIO()
     assert cli_main(["--help"], out, io.StringIO()) == 0
     assert "model" in out.getvalue()
+
+
+def test_model_with_rho_matches_reference(tmp_path, oracle_ref, mm):
+    """save_model / load_model with a density volume (model.cpp:122-184): the
+    acoustic_iso engine's model files."""
+    n = (5, 6, 7)
+    g = mm.make_grid(n, (10.0, 12.0, 14.0))
+    rng = np.random.default_rng(9)
+    vp, rho = g.field(), g.field()
+    g.inner(vp)[...] = rng.uniform(1500, 4000, n).astype(np.float32)
+    g.inner(rho)[...] = rng.uniform(900, 2600, n).astype(np.float32)
+    model = mm.validate_model(mm.EarthModel(g, vp, rho=rho))
+    (tmp_path / "ours").mkdir()
+    (tmp_path / "ref").mkdir()
+    shotio.save_model(model, tmp_path / "ours" / "m.json")
+    oracle_ref.save_model_rho(model.vp, model.rho, n, g.d, 4, tmp_path / "ref" / "m.json")
+    for f in ("vp.f32", "rho.f32", "m.json"):
+        assert (tmp_path / "ours" / f).read_bytes() == (tmp_path / "ref" / f).read_bytes(), f
+    back = shotio.load_model(tmp_path / "ref" / "m.json")
+    assert np.array_equal(back.rho, oracle_ref.load_model_rho(tmp_path / "ref" / "m.json", n))
+    assert np.array_equal(back.rho, model.rho) and np.array_equal(back.vp, model.vp)
+    (tmp_path / "ours" / "rho.f32").write_bytes(b"\0" * 8)
+    with pytest.raises(ConfigError, match="size mismatch"):
+        shotio.load_model(tmp_path / "ours" / "m.json")
