@@ -432,8 +432,8 @@ def run_vd(args):
                 "d2h_bytes_per_step": 4 * nrec},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "kernel": dominant, "algorithmic_bytes_per_launch": kb[dominant],
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(f"vd_{edge}^3", dominant), "kernel": dominant, "algorithmic_bytes_per_launch": kb[dominant],
                      "kernel_ms": round(kms[dominant], 4), "peak_source": peak_src},
         "kernels": {k: {"ms": round(kms[k], 4), "algorithmic_bytes": kb[k],
                         "achieved_gbs": round(kb[k] / (kms[k] * 1e-3) / 1e9, 1)} for k in kms},
@@ -475,7 +475,8 @@ def run_reference(args):
         "config": {"workload": f"{args.propagator} r=4 {n[0]}x{n[1]}x{n[2]} grid, nd=27 CPML, "
                                f"taper (bounded sample: {ns} steps from t=0)", "grid": list(n)},
         "cpu_baseline": {"value": round(gpts, 5), "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{n[0]}x{n[1]}x{n[2]} x {ns} steps, run() Target::Parallel"},
+                         "sample": f"{n[0]}x{n[1]}x{n[2]} x {ns} steps, run("
+                                   f"{'AcousticIso' if vd else 'AcousticIsoCd'}) Target::Parallel"},
         "e2e": {"value": round(gpts, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
