@@ -163,8 +163,10 @@ int mm_cd_set_receivers(mm_cd_engine* e, const int* ijk, int nreceivers, int cap
 int mm_cd_record(mm_cd_engine* e, int step);
 int mm_cd_get_traces(mm_cd_engine* e, float* host, int nsteps);
 /* Copy one recorded time sample (all receivers, nreceivers floats, receiver
- * order) to host memory.  async != 0: enqueue on the engine stream and
- * return (host should be pinned; read it after mm_cd_synchronize). */
+ * order) to host memory.  async != 0: enqueue on the engine's copy stream,
+ * ordered after the work enqueued so far, and return -- the copy overlaps the
+ * following steps (host should be pinned; read it after mm_cd_synchronize,
+ * which also waits for the copy stream). */
 int mm_cd_copy_trace_step(mm_cd_engine* e, int step, float* host, int async);
 
 /* Device-resident time loop: nsteps steps with source amplitudes amps[]

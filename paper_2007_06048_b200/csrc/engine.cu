@@ -89,6 +89,7 @@ struct mm_cd_engine {
     DevBuf<float> traces;
     int nrec = 0, cap = 0;
     DevBuf<int> counters;  // [0] step counter, [1] first bad step
+    TraceCopier tcopy;
     DevBuf<float> amps;
     long long steps = 0;
     std::unique_ptr<FastPlan> fast;
@@ -553,6 +554,7 @@ int mm_cd_synchronize(mm_cd_engine* e) {
     MM_API_BEGIN
     use(e);
     MM_CUDA(cudaStreamSynchronize(e->stream));
+    e->tcopy.sync();
     MM_API_END
 }
 
@@ -714,9 +716,15 @@ int mm_cd_copy_trace_step(mm_cd_engine* e, int step, float* host, int async) {
     need(host, "host");
     if (step < 0 || step >= e->cap) raise(ST_INVAL, "step outside the trace capacity");
     if (e->nrec == 0) return MM_OK;
+    if (async) {
+        // off the compute stream: the copy overlaps the next step
+        e->tcopy.copy(host, e->traces.ptr + (size_t)step * e->nrec, sizeof(float) * e->nrec,
+                      e->stream);
+        return MM_OK;
+    }
     MM_CUDA(cudaMemcpyAsync(host, e->traces.ptr + (size_t)step * e->nrec,
                             sizeof(float) * e->nrec, cudaMemcpyDeviceToHost, e->stream));
-    if (!async) MM_CUDA(cudaStreamSynchronize(e->stream));
+    MM_CUDA(cudaStreamSynchronize(e->stream));
     MM_API_END
 }
 

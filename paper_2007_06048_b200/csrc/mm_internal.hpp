@@ -125,6 +125,33 @@ struct DevBuf {
     }
 };
 
+// Asynchronous device->host copies of recorded receiver samples on their own
+// stream, ordered after the recording kernel by an event, so the copy engine
+// overlaps the next step's kernels instead of stalling the compute stream.
+struct TraceCopier {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev = nullptr;
+    void copy(void* dst, const void* src, size_t bytes, cudaStream_t after) {
+        if (!cs) {
+            MM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            MM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        }
+        MM_CUDA(cudaEventRecord(ev, after));
+        MM_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        MM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
+    }
+    void sync() {
+        if (cs) MM_CUDA(cudaStreamSynchronize(cs));
+    }
+    ~TraceCopier() {
+        if (cs) {
+            cudaStreamSynchronize(cs);
+            cudaStreamDestroy(cs);
+        }
+        if (ev) cudaEventDestroy(ev);
+    }
+};
+
 struct Layout {
     int n[3];
     int r, L, P, ey, ez;

@@ -333,6 +333,7 @@ struct mm_vd_engine {
     DevBuf<float> traces;
     int nrec = 0, cap = 0;
     DevBuf<int> counters;  // [0] step counter, [1] first bad step
+    TraceCopier tcopy;
     DevBuf<float> amps;
     long long steps = 0;
     int zc = 32;
@@ -653,6 +654,7 @@ int mm_vd_synchronize(mm_vd_engine* e) {
     MM_API_BEGIN
     use(e);
     MM_CUDA(cudaStreamSynchronize(e->stream));
+    e->tcopy.sync();
     MM_API_END
 }
 
@@ -766,9 +768,15 @@ int mm_vd_copy_trace_step(mm_vd_engine* e, int step, float* host, int async) {
     need(host, "host");
     if (step < 0 || step >= e->cap) raise(ST_INVAL, "step outside the trace capacity");
     if (e->nrec == 0) return MM_OK;
+    if (async) {
+        // off the compute stream: the copy overlaps the next step
+        e->tcopy.copy(host, e->traces.ptr + (size_t)step * e->nrec, sizeof(float) * e->nrec,
+                      e->stream);
+        return MM_OK;
+    }
     MM_CUDA(cudaMemcpyAsync(host, e->traces.ptr + (size_t)step * e->nrec,
                             sizeof(float) * e->nrec, cudaMemcpyDeviceToHost, e->stream));
-    if (!async) MM_CUDA(cudaStreamSynchronize(e->stream));
+    MM_CUDA(cudaStreamSynchronize(e->stream));
     MM_API_END
 }
 
