@@ -256,6 +256,11 @@ struct FastVd {
         ctr.alloc_zero(4, s);
         grid_v = std::min(nitems, sms * ov);
         grid_p = std::min(nitems, sms * op);
+        // MM_VD_CTAS (diagnostics): cap the CTA count (long item sequences per CTA)
+        if (const char* e = std::getenv("MM_VD_CTAS")) {
+            grid_v = std::min(grid_v, std::max(1, std::atoi(e)));
+            grid_p = std::min(grid_p, std::max(1, std::atoi(e)));
+        }
     }
 
     void launch(bool velocity, vdk::VdFastParams P, cudaStream_t s) {

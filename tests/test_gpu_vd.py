@@ -204,3 +204,41 @@ def test_vd_kernel_families_agree(mm, monkeypatch):
         assert np.array_equal(fast.velocity(ax), plain.velocity(ax))
     fast.close()
     plain.close()
+
+
+@pytest.mark.parametrize("ctas", ["1", "7"])
+def test_vd_few_ctas(ctas, tmp_path):
+    """Long item sequences per CTA through the TMA rings (MM_VD_CTAS, read at
+    engine creation) on an odd free-surface grid: still bit-identical to the
+    plain kernels."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    script = tmp_path / "vd_few.py"
+    script.write_text(
+        "import os, sys, numpy as np\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import paper_2007_06048_b200 as mm\n"
+        "n = (61, 47, 53)\n"
+        "g = mm.make_grid(n, (20.0, 15.0, 10.0), 4)\n"
+        "rng = np.random.default_rng(5)\n"
+        "vp, rho = g.field(), g.field()\n"
+        "g.inner(vp)[...] = rng.uniform(1500, 4500, n).astype(np.float32)\n"
+        "g.inner(rho)[...] = rng.uniform(1000, 2500, n).astype(np.float32)\n"
+        "m = mm.validate_model(mm.EarthModel(g, vp, rho=rho))\n"
+        "o = mm.EngineOptions(ndamping=(9, 7, 11), taper=True, free_surface=True)\n"
+        "w = mm.integrate_wavelet(mm.ricker(25.0, 1e-3, 40)).samples\n"
+        "fast = mm.AcousticVdEngine(g, m, o, 1e-3)\n"
+        "os.environ['MM_VD_SIMPLE'] = '1'\n"
+        "plain = mm.AcousticVdEngine(g, m, o, 1e-3)\n"
+        "for s in range(40):\n"
+        "    fast.step(float(w[s]) * 1e6, (30, 23, 26))\n"
+        "    plain.step(float(w[s]) * 1e6, (30, 23, 26))\n"
+        "assert np.array_equal(fast.pressure(), plain.pressure())\n"
+        "assert all(np.array_equal(fast.velocity(a), plain.velocity(a)) for a in range(3))\n"
+        "print('ok')\n")
+    env = dict(os.environ, MM_VD_CTAS=ctas)
+    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

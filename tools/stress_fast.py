@@ -1,6 +1,7 @@
 """Stress the fast acoustic_iso_cd step under concurrency (diagnostics).
 
-    MODES=fast[,strict|,fast] BUSY=0|1 FS=0|1 python tools/stress_fast.py ITERATIONS
+    MODES=fast[,strict|,fast] BUSY=0|1 FS=0|1 [N=nx,ny,nz ND=a,b,c R=4] \
+        python tools/stress_fast.py ITERATIONS
 
 Runs the odd-extent free-surface configuration of test_gpu_parity for
 ITERATIONS fresh engines, optionally interleaved with other engines (MODES)
@@ -11,7 +12,13 @@ whose final field differs from the first one.  Combine with MM_BND_CTAS=<n>
 import os, sys, numpy as np
 sys.path.insert(0,'.')
 import paper_2007_06048_b200 as mm
-n, nd, radius, src = (61, 47, 53), (9, 7, 11), 4, (30, 23, 40)
+def _t(k, d):
+    v = os.environ.get(k)
+    return tuple(int(x) for x in v.split(",")) if v else d
+n = _t("N", (61, 47, 53))
+nd = _t("ND", (9, 7, 11))
+radius = int(os.environ.get("R", "4"))
+src = tuple(x // 2 for x in n)
 fs = os.environ.get("FS", "1") == "1"
 modes = os.environ.get("MODES", "fast,strict").split(",")
 steps, dt = 60, 1.0e-3
