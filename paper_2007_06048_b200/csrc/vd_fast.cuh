@@ -49,11 +49,23 @@ struct VdCfg {
     static constexpr int TILE = pad32(TX * TY);
     // velocity: p halo planes, ring = z window 2R + lead
     static constexpr int PPLANE = pad32(BX * BY);
-    static constexpr int NSV = 2 * R + 1;
-    static constexpr int NQV = R <= 4 ? 3 : 2;  // dt/rho + v stages
+#ifndef MM_VD_LEADV
+#define MM_VD_LEADV 1
+#endif
+#ifndef MM_VD_NQV
+#define MM_VD_NQV 3
+#endif
+#ifndef MM_VD_LEADP
+#define MM_VD_LEADP 2
+#endif
+#ifndef MM_VD_NQP
+#define MM_VD_NQP 3
+#endif
+    static constexpr int NSV = 2 * R + MM_VD_LEADV;
+    static constexpr int NQV = R <= 4 ? MM_VD_NQV : 2;  // dt/rho + v stages
     // pressure: vz tiles (z window 2R + lead), vx / vy halo boxes + dtb + p (NQ stages)
-    static constexpr int NSP = 2 * R + 2;
-    static constexpr int NQP = 3;
+    static constexpr int NSP = 2 * R + MM_VD_LEADP;
+    static constexpr int NQP = MM_VD_NQP;
     static constexpr int VXB = pad32(BX * TY), VYB = pad32(TX * BY);
     static constexpr size_t SMEM_V =
         sizeof(float) * (size_t)(NSV * PPLANE + NQV * 4 * TILE) + 8 * (NSV + NQV) + 16;

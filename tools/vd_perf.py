@@ -36,8 +36,24 @@ def main(edges):
         t = ms / steps
         N = edge ** 3
         B = bytes_per_step(n, nd)
+        # per-kernel device times (sub-phases back to back, CUDA events)
+        import torch
+        ext = torch.cuda.ExternalStream(e.stream_handle())
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        kv = kp = 0.0
+        reps = 20
+        for _ in range(reps):
+            ev[0].record(ext)
+            e.update_velocity()
+            ev[1].record(ext)
+            e.update_pressure()
+            ev[2].record(ext)
+            torch.cuda.synchronize()
+            kv += ev[0].elapsed_time(ev[1]) / reps
+            kp += ev[1].elapsed_time(ev[2]) / reps
         print(f"{edge}^3: {t*1e3:.1f} us/step  {N/t/1e6:.1f} Gpts/s  "
-              f"{B/t/1e6:.0f} GB/s (model {B/N:.1f} B/pt)")
+              f"{B/t/1e6:.0f} GB/s (model {B/N:.1f} B/pt)  velocity {kv*1e3:.1f} us  "
+              f"pressure {kp*1e3:.1f} us")
         e.close()
 
 
