@@ -238,12 +238,15 @@ struct FastVd {
         MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ov, vdk::k_vdv<R>, C::NT, C::SMEM_V));
         MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&op, vdk::k_vdp<R>, C::NT, C::SMEM_P));
         if (ov < 1 || op < 1) raise(ST_CUDA, "acoustic_iso kernels do not fit on an SM");
-        // (tile, z-chunk) items, chunk-major; about 6 items per resident CTA
-        // (measured at 240^3: 4 -> 6 items per CTA +1.3 %, 2 -> 4 +12 %)
+        // (tile, z-chunk) items, chunk-major, short enough that the tiles in
+        // flight stay at nearby depths (their halo planes meet in L2): about
+        // 20 planes per item and at least ~6 items per resident CTA.
+        // Measured: 1000^3 59 -> 93 Gpts/s going from 500- to 20-plane items,
+        // 512^3 76 -> 89 (73 -> 16 planes); 240^3 best at 8-12 planes.
         const int tx = (L.n[0] + C::TX - 1) / C::TX, ty = (L.n[1] + C::TY - 1) / C::TY;
         const int slots = sms * std::max(ov, op);
-        int nch = std::max(1, (6 * slots + tx * ty - 1) / (tx * ty));
-        nch = std::min(nch, std::max(1, L.n[2] / 8));
+        int nch = std::max((L.n[2] + 19) / 20, (6 * slots + tx * ty - 1) / (tx * ty));
+        nch = std::max(1, std::min(nch, std::max(1, L.n[2] / 8)));
         if (const char* e = std::getenv("MM_VD_ZCHUNKS")) nch = std::max(1, std::atoi(e));
         std::vector<int4> it;
         for (int c = 0; c < nch; ++c) {

@@ -242,3 +242,29 @@ def test_vd_few_ctas(ctas, tmp_path):
     r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.slow
+def test_vd_large_grid_families_agree(mm, monkeypatch):
+    """1000 x 1000 x 120 (byte offsets past 2^32 per field, 32 x 32 tiles with
+    a partial last column): TMA kernels == plain kernels after a few steps
+    from a random pressure field with every damping run active."""
+    n = (1000, 1000, 120)
+    g = mm.make_grid(n, (20.0, 20.0, 20.0), 4)
+    model = mm.default_layered_model(g)
+    opts = mm.EngineOptions(ndamping=(27, 27, 27), free_surface=True)
+    rng = np.random.default_rng(8)
+    p0 = g.field()
+    g.inner(p0)[...] = rng.standard_normal(n).astype(np.float32)
+    fast = mm.AcousticVdEngine(g, model, opts, 1e-3)
+    monkeypatch.setenv("MM_VD_SIMPLE", "1")
+    plain = mm.AcousticVdEngine(g, model, opts, 1e-3)
+    monkeypatch.delenv("MM_VD_SIMPLE")
+    for e in (fast, plain):
+        e.set_pressure(p0)
+        for s in range(3):
+            e.step(1.0, (500, 500, 60))
+    assert np.array_equal(fast.pressure(), plain.pressure())
+    assert np.array_equal(fast.velocity(0), plain.velocity(0))
+    fast.close()
+    plain.close()
