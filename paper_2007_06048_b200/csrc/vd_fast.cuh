@@ -41,8 +41,12 @@ template <int R>
 struct VdCfg {
     static constexpr int TXT = 8;          // threads per row, 4 x-points each
     static constexpr int TX = 4 * TXT;     // 32
-    static constexpr int TY = 32;          // rows (one per thread row)
+#ifndef MM_VD_TY
+#define MM_VD_TY 32
+#endif
+    static constexpr int TY = MM_VD_TY;    // rows (one per thread row)
     static constexpr int NT = TXT * TY;    // 256
+    static constexpr int MINB = TY >= 32 ? 2 : 4;  // CTAs per SM the registers allow
     static constexpr int HX = R <= 4 ? 4 : 8;  // x halo (float4 granules)
     static constexpr int BX = TX + 2 * HX;
     static constexpr int BY = TY + 2 * R;
@@ -258,7 +262,7 @@ struct VdvMaps {
 };
 
 template <int R>
-__global__ void __launch_bounds__(VdCfg<R>::NT, 2)
+__global__ void __launch_bounds__(VdCfg<R>::NT, VdCfg<R>::MINB)
     k_vdv(const __grid_constant__ VdvMaps M, const VdFastParams P) {
     using C = VdCfg<R>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -404,7 +408,7 @@ struct VdpMaps {
 };
 
 template <int R>
-__global__ void __launch_bounds__(VdCfg<R>::NT, 2)
+__global__ void __launch_bounds__(VdCfg<R>::NT, VdCfg<R>::MINB)
     k_vdp(const __grid_constant__ VdpMaps M, const VdFastParams P) {
     using C = VdCfg<R>;
     constexpr int QST = C::VXB + C::VYB + 2 * C::TILE;  // floats per stage
