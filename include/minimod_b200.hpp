@@ -1,6 +1,7 @@
 // minimod_b200.hpp -- header-only C++ drop-in over the C ABI (minimod_b200.h).
 //
-// Same shape as the reference's minimod::AcousticCdEngine<float>
+// AcousticVdEngine (acoustic_iso) follows at the end.  AcousticCdEngine has
+// the same shape as the reference's minimod::AcousticCdEngine<float>
 // (propagator.hpp:93-140): construct from a ghosted z-fastest vp field,
 // step(amp, src), pressure(), pressure_prev(), set_state(), profile().  Status
 // codes are rethrown as the reference's exception types (errors.hpp:10-30).
@@ -138,6 +139,64 @@ private:
     Grid grid_;
     std::array<int, 3> global_n_;
     mm_cd_engine* h_ = nullptr;
+};
+
+// ref: propagator.hpp:147-176 AcousticVdEngine<float> (acoustic_iso).  vp and
+// rho are the model's ghosted z-fastest volumes; rho == nullptr reproduces the
+// reference's ValidationError.  pressure()/velocity() return host copies; the
+// reference's mutable references map to set_pressure()/set_velocity().
+class AcousticVdEngine {
+public:
+    AcousticVdEngine(const Grid& g, const std::vector<float>& vp, const std::vector<float>* rho,
+                     const EngineOptions& o, float dt, double vmax, int device = 0)
+        : grid_(g) {
+        if (vp.size() != g.volume() || (rho && rho->size() != g.volume()))
+            throw std::invalid_argument("model volumes do not match the ghosted grid");
+        mm_grid cg{{g.n[0], g.n[1], g.n[2]}, {g.d[0], g.d[1], g.d[2]}, g.radius};
+        mm_engine_options co{{o.ndamping[0], o.ndamping[1], o.ndamping[2]},
+                             o.fmax,
+                             o.r_target,
+                             o.free_surface ? 1 : 0,
+                             o.taper ? 1 : 0,
+                             {o.ntaper[0], o.ntaper[1], o.ntaper[2]}};
+        check(mm_vd_create(&cg, vp.data(), rho ? rho->data() : nullptr, &co, dt, vmax, device,
+                           &h_));
+    }
+    ~AcousticVdEngine() {
+        if (h_) mm_vd_destroy(h_);
+    }
+    AcousticVdEngine(const AcousticVdEngine&) = delete;
+    AcousticVdEngine& operator=(const AcousticVdEngine&) = delete;
+
+    // ref: propagator.hpp:154-155 (amp: the time-integrated wavelet sample)
+    void step(float amp, std::optional<std::array<int, 3>> src) {
+        check(mm_vd_step(h_, amp, src ? src->data() : nullptr));
+    }
+    std::vector<float> pressure() const {
+        std::vector<float> out(grid_.volume());
+        check(mm_vd_get_pressure(h_, out.data()));
+        return out;
+    }
+    std::vector<float> velocity(int axis) const {
+        std::vector<float> out(grid_.volume());
+        check(mm_vd_get_velocity(h_, axis, out.data()));
+        return out;
+    }
+    void set_pressure(const std::vector<float>& p) { check(mm_vd_set_pressure(h_, p.data())); }
+    void set_velocity(int axis, const std::vector<float>& v) {
+        check(mm_vd_set_velocity(h_, axis, v.data()));
+    }
+    const Grid& grid() const { return grid_; }
+    float dt() const {
+        float v = 0;
+        check(mm_vd_get_dt(h_, &v));
+        return v;
+    }
+    mm_vd_engine* handle() { return h_; }
+
+private:
+    Grid grid_;
+    mm_vd_engine* h_ = nullptr;
 };
 
 }  // namespace minimod_b200

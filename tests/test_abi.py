@@ -44,6 +44,7 @@ def test_cxx_header_compiles(tmp_path):
         pytest.skip("no g++")
     src = tmp_path / "t.cpp"
     src.write_text('#include "minimod_b200.hpp"\nint main(){ minimod_b200::EngineOptions o; '
+                   'minimod_b200::AcousticVdEngine* e = nullptr; (void)e; '
                    'return o.ndamping[0]; }\n')
     res = subprocess.run([gxx, "-std=c++17", "-fsyntax-only", f"-I{ROOT / 'include'}", str(src)],
                          capture_output=True, text=True)
