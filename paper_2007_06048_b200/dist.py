@@ -395,6 +395,13 @@ def bench_rank(args, rank, world, local):
 
     torch.cuda.set_device(local)
     if not dist.is_initialized():
+        if "RANK" not in os.environ:  # a single rank started without torchrun
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK=str(local),
+                              MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     edge = args.grid or 240
     n = (edge, edge, edge * world)
