@@ -495,17 +495,36 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
 
                 // reference: drive = d2p*ik + dpsi; zeta = b*zeta + a*drive;
                 // term = drive + zeta; lap = (term_x + term_y) + term_z
-                float out[4], nzx[4], nzy[4], nzz[4];
+                float out[4], drx[4], dry[4], drz[4];
+                float nzx[4] = {0.f, 0.f, 0.f, 0.f}, nzy[4] = {0.f, 0.f, 0.f, 0.f},
+                      nzz[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const float drx = acc<ORD>(dpx[e], d2x[e], axk[e]);
-                    const float dry = acc<ORD>(dpy[e], d2y[e], ayk);
-                    const float drz = acc<ORD>(comp(dz, e), d2z[e], azk);
-                    nzx[e] = fx ? acc<ORD>(fm<ORD>(axa[e], drx), axb[e], comp(zx, e)) : 0.f;
-                    nzy[e] = y_in_zy ? acc<ORD>(fm<ORD>(aya, dry), ayb, comp(zy, e)) : 0.f;
-                    nzz[e] = zr >= 0 ? acc<ORD>(fm<ORD>(aza, drz), azb, comp(zz, e)) : 0.f;
-                    const float lap = fa<ORD>(fa<ORD>(fa<ORD>(drx, nzx[e]), fa<ORD>(dry, nzy[e])),
-                                              fa<ORD>(drz, nzz[e]));
+                    drx[e] = acc<ORD>(dpx[e], d2x[e], axk[e]);
+                    dry[e] = acc<ORD>(dpy[e], d2y[e], ayk);
+                    drz[e] = acc<ORD>(comp(dz, e), d2z[e], azk);
+                }
+                // zeta updates only where a run holds the row / plane (uniform
+                // branches: no FP spent on the other tiles' terms)
+                if (fx) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        nzx[e] = acc<ORD>(fm<ORD>(axa[e], drx[e]), axb[e], comp(zx, e));
+                }
+                if (y_in_zy) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        nzy[e] = acc<ORD>(fm<ORD>(aya, dry[e]), ayb, comp(zy, e));
+                }
+                if (zr >= 0) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        nzz[e] = acc<ORD>(fm<ORD>(aza, drz[e]), azb, comp(zz, e));
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float lap = fa<ORD>(fa<ORD>(fa<ORD>(drx[e], nzx[e]), fa<ORD>(dry[e], nzy[e])),
+                                              fa<ORD>(drz[e], nzz[e]));
                     out[e] = acc<ORD>(fs<ORD>(two_p0[e], comp(pp, e)), comp(cv, e), lap);
                 }
                 // stores: p_next inside the box, zeta where a run holds the point
