@@ -334,8 +334,7 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                 if (lane == 0) mbar_arrive_b(emptyP + 8 * rel);
                 if (++rel == C::NS) rel = 0;
             }
-            continue;
-        }
+        } else {
 #pragma unroll 1
         for (int j = 0; j < T.nring; ++j) {
             const int s = np % C::NS;
@@ -410,6 +409,7 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
             __syncwarp();
             if (lane == 0) mbar_arrive_b(emptyP + 8 * ((np + C::NS - k) % C::NS));
         }
+        }  // if constexpr (Z)
     }
 }
 
