@@ -127,8 +127,12 @@ struct TileCfg {
         xside = B.kind == 0 ? B.side : -1;
         fx = xside >= 0 && P.run[0][xside].hi > P.run[0][xside].lo;
         const bool usey = B.kind <= 1;  // dpsi_y only in X and Y slabs
-        fy0 = usey && near_run(P.run[1][0], y0 - R, y0 + C::TY + R);
-        fy1 = usey && near_run(P.run[1][1], y0 - R, y0 + C::TY + R);
+        // an X slab spans every y and sees both y runs; a Y slab box holds its
+        // own run only (the other is zero halo even within R of it)
+        fy0 = usey && (B.kind == 0 || B.side == 0) &&
+              near_run(P.run[1][0], y0 - R, y0 + C::TY + R);
+        fy1 = usey && (B.kind == 0 || B.side == 1) &&
+              near_run(P.run[1][1], y0 - R, y0 + C::TY + R);
         int o = 2 * C::TILE, b = 2 * C::TILE_N;
         o_psx = o;
         if (fx) o += C::PSX, b += C::PSX_N;
@@ -155,6 +159,12 @@ __device__ __forceinline__ int zrun_of(const BndParams& P, int z) {
 // z run whose dpsi_z planes hold z (the ranges never overlap: see kernels_fast.cu)
 __device__ __forceinline__ int zext_of(const BndParams& P, int z) {
     return z >= P.dz_lo[0] && z < P.dz_hi[0] ? 0 : z >= P.dz_lo[1] && z < P.dz_hi[1] ? 1 : -1;
+}
+// ... as seen from box B: a Z slab box holds its own z layer only, so the other
+// run's dpsi_z (within R of it when the inner z extent is < R) is zero halo there
+__device__ __forceinline__ int zext_in(const BndParams& P, int z, const BndBox& B) {
+    const int e = zext_of(P, z);
+    return B.kind == 2 && e != B.side ? -1 : e;
 }
 // Circular stage allocation (identical on both sides): a stage never wraps.
 __device__ __forceinline__ uint32_t q_alloc(uint32_t& V, int size, int qb) {
@@ -252,7 +262,7 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                 const TileCfg<R> T(P, sg);
                 for (int oq = 0; oq < T.nout; ++oq) {
                     const int z = T.zb + oq;
-                    const int zr = zrun_of(P, z), ze = zext_of(P, z);
+                    const int zr = zrun_of(P, z), ze = zext_in(P, z, T.B);
                     const int size = T.qsize + (zr >= 0 ? C::TILE : 0) + (ze >= 0 ? C::TILE : 0);
                     const uint32_t vn = q_alloc(V, size, C::QB);
                     // free: stage nq - NQD (barrier reuse) and every stage whose space
@@ -382,7 +392,7 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                 const int z = T.zb + o;
                 const long long fo = (long long)o * L.plane;
                 const int zr = zrun_of(P, z);
-                const int zex = zext_of(P, z);
+                const int zex = zext_in(P, z, T.B);
                 float* zz_p = (zr == 0 ? zzb0 : zzb1) + o * zz_step;
                 const float aza = __ldg(P.ta[2] + z), azb = __ldg(P.tb[2] + z),
                             azk = __ldg(P.tik[2] + z);

@@ -58,6 +58,7 @@ struct InnerParams {
     // here too, with the CPML pass-2 formula along z (update_damping_pass2,
     // propagator_impl.hpp:125-152): dpsi_z from k_p1, zeta_z in the z runs.
     int zi_lo, zi_hi;
+    int zsplit;  // first local plane of the high z layer (a Z slab sees its own run only)
     const float* tik_x;
     const float* tik_y;
     const float* ta_z;
@@ -346,9 +347,10 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, 1)
             const int z = zb + o;
             if (z >= P.zi_lo && z < P.zi_hi) return;  // inner plane: plain update
             const int zr = zrun_at(z);
-            const int ze2 = z >= P.dz_lo[0] && z < P.dz_hi[0]   ? 0
-                            : z >= P.dz_lo[1] && z < P.dz_hi[1] ? 1
-                                                                : -1;
+            int ze2 = z >= P.dz_lo[0] && z < P.dz_hi[0]   ? 0
+                      : z >= P.dz_lo[1] && z < P.dz_hi[1] ? 1
+                                                          : -1;
+            if (ze2 != (z >= P.zsplit ? 1 : 0)) ze2 = -1;  // the other layer is halo
             zz = make_float4(0.f, 0.f, 0.f, 0.f);
             dz = zz;
             if (yok) {

@@ -545,6 +545,7 @@ private:
         ip.center = -2.0f * sum;
         ip.zi_lo = w.box.lo[2];
         ip.zi_hi = w.box.hi[2];
+        ip.zsplit = p.gn[2] - p.nd[2] - p.goff[2];
         ip.tik_x = p.tik[0];
         ip.tik_y = p.tik[1];
         ip.ta_z = p.ta[2];

@@ -42,12 +42,17 @@ __device__ __forceinline__ const CpmlRun* run_at(const StepParams& p, int ax, in
 }
 
 // psi_ax at local (i,j,k) shifted by `sh` along ax; zero outside the damping
-// runs and outside the local box (the reference's zero halo).
-__device__ __forceinline__ float psi_at(const StepParams& p, int ax, int i, int j, int k, int sh) {
+// runs and outside the local box (the reference's zero halo).  With `only`,
+// `own` is the one run the point's slab box holds along ax (nullptr: none
+// active): a slab of axis ax spans just its own layer, so the opposite layer
+// is halo there even when it lies within R (inner extent < R), while slabs of
+// an earlier axis span the whole of ax and see both layers.
+__device__ __forceinline__ float psi_at(const StepParams& p, int ax, int i, int j, int k, int sh,
+                                        bool only, const CpmlRun* own) {
     int loc[3] = {i, j, k};
     loc[ax] += sh;
     const CpmlRun* r = run_at(p, ax, loc[ax]);
-    if (!r) return 0.0f;
+    if (!r || (only && r != own)) return 0.0f;
     return __ldg(r->psi + run_off(*r, ax, loc[0], loc[1], loc[2]));
 }
 
@@ -79,6 +84,7 @@ __global__ void k_strict_update(StepParams p, int region, int z_lo) {
         // inner x range; Z slabs the inner x,y range.  dpsi_ax reads psi only
         // inside the point's own slab box, which is what these masks encode.
         const bool use[3] = {!in[0], !in[0] || !in[1], true};
+        const int sa = !in[0] ? 0 : !in[1] ? 1 : 2;  // the axis of the point's slab
         const int loc[3] = {i, j, k};
         float term[3];
 #pragma unroll
@@ -89,10 +95,13 @@ __global__ void k_strict_update(StepParams p, int region, int z_lo) {
                         ik = __ldg(p.tik[ax] + l);
             float dpsi = 0.0f;
             if (use[ax]) {
+                const bool only = ax == sa;
+                const CpmlRun* own = only ? run_at(p, ax, l) : nullptr;
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
-                    dpsi = fadd(dpsi, fmul(p.c1[ax][m - 1], fsub(psi_at(p, ax, i, j, k, m),
-                                                                 psi_at(p, ax, i, j, k, -m))));
+                    dpsi = fadd(dpsi,
+                                fmul(p.c1[ax][m - 1], fsub(psi_at(p, ax, i, j, k, m, only, own),
+                                                           psi_at(p, ax, i, j, k, -m, only, own))));
             }
             const float drive = fadd(fmul(d2p, ik), dpsi);
             const CpmlRun* run = run_at(p, ax, l);

@@ -355,3 +355,61 @@ def test_fast_boundary_few_ctas_regression(ctas, tmp_path):
     r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n,nd,radius,fs", [
+    ((5, 7, 9), (1, 2, 3), 4, True),     # smaller than one tile; inner extent < R
+    ((5, 7, 9), (1, 2, 3), 4, False),    # ... both z layers active and within R
+    ((1, 40, 33), (0, 6, 5), 2, True),   # a single x column
+    ((37, 1, 12), (8, 0, 2), 4, True),   # a single y row
+    ((20, 18, 2), (4, 3, 0), 8, True),   # two z planes, r = 8
+    ((9, 9, 9), (4, 4, 4), 4, True),     # inner box of one point
+    ((9, 9, 9), (4, 4, 4), 4, False),
+    ((40, 12, 40), (6, 5, 6), 4, False),  # y layers 2 apart: a Y slab sees only its own
+])
+def test_tiny_and_degenerate_grids_vs_oracle(mm, oracle_port, n, nd, radius, fs):
+    """Grids whose damping layers lie within R of each other: a slab box of
+    axis a holds only its own layer's CPML memory along a (the other layer is
+    zero halo, cpml.hpp:77-99), slabs of an earlier axis see both layers."""
+    h = (20.0, 15.0, 10.0)
+    grid = mm.make_grid(n, h, radius)
+    m = mm.random_model(grid, seed=2)
+    w = mm.ricker(25.0, 1e-3, 15).samples
+    opts = mm.EngineOptions(ndamping=nd, taper=True, free_surface=fs)
+    src = tuple(x // 2 for x in n)
+    ref = oracle_port.engine(n, m.vp, d=h, radius=radius, ndamping=nd, free_surface=fs,
+                             taper=True, dt=1e-3, vmax=m.vmax)
+    eng = {md: mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax, mode=md)
+           for md in ("fast", "strict")}
+    for s in range(15):
+        ref.step(float(w[s]) * 1e3, src)
+        for e in eng.values():
+            e.step(float(w[s]) * 1e3, src)
+    want = ref.pressure().reshape(grid.shape)
+    assert np.abs(want).max() > 0
+    for md, e in eng.items():
+        assert np.array_equal(e.pressure(), want), md
+
+
+@pytest.mark.parametrize("zslabs", ["0", "1", "2"])
+@pytest.mark.parametrize("n,nd", [((5, 7, 9), (1, 2, 3)), ((9, 9, 9), (4, 4, 4)),
+                                  ((24, 20, 7), (5, 4, 3))])
+def test_tiny_grids_every_zslab_schedule(mm, oracle_port, monkeypatch, zslabs, n, nd):
+    """Free surface (low z layer inactive) with the high z run within R of the
+    low Z slab: each Z-slab schedule (k_bnd tiles, k_zslab after k_inner,
+    k_zslab over whole columns) keeps the other run's dpsi_z out of it."""
+    monkeypatch.setenv("MM_ZSLABS", zslabs)
+    h = (20.0, 15.0, 10.0)
+    grid = mm.make_grid(n, h, 4)
+    m = mm.random_model(grid, seed=5)
+    w = mm.ricker(25.0, 1e-3, 15).samples
+    src = tuple(x // 2 for x in n)
+    ref = oracle_port.engine(n, m.vp, d=h, ndamping=nd, free_surface=True, taper=True,
+                             dt=1e-3, vmax=m.vmax)
+    e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp,
+                            mm.EngineOptions(ndamping=nd, taper=True, free_surface=True),
+                            1e-3, m.vmax, mode="fast")
+    for s in range(15):
+        ref.step(float(w[s]) * 1e3, src)
+        e.step(float(w[s]) * 1e3, src)
+    assert np.array_equal(e.pressure(), ref.pressure().reshape(grid.shape))

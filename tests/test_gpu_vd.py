@@ -268,3 +268,28 @@ def test_vd_large_grid_families_agree(mm, monkeypatch):
     assert np.array_equal(fast.velocity(0), plain.velocity(0))
     fast.close()
     plain.close()
+
+
+@pytest.mark.parametrize("n,r,nd,fs", [
+    ((5, 7, 9), 4, (1, 2, 3), True),     # smaller than one tile, thinner than the halo
+    ((5, 7, 9), 4, (1, 2, 3), False),    # both z layers active and within R
+    ((1, 40, 33), 2, (0, 6, 5), True),   # a single x column
+    ((37, 1, 12), 3, (8, 0, 2), True),   # a single y row
+    ((20, 18, 2), 8, (4, 3, 0), True),   # two z planes, r = 8
+    ((9, 9, 9), 4, (4, 4, 4), False),    # inner box of one point
+    ((40, 12, 40), 4, (6, 5, 6), False),  # y layers 2 apart
+])
+def test_vd_tiny_and_degenerate_grids(mm, oracle_port, n, r, nd, fs):
+    g, m = _model(mm, n, r, seed=sum(n) + r)
+    dt = 5e-4
+    src = tuple(x // 2 for x in n)
+    w = mm.integrate_wavelet(mm.ricker(25.0, dt, 12)).samples
+    o = oracle_port.vd_engine(n, m.vp, m.rho, radius=r, ndamping=nd, free_surface=fs,
+                              dt=dt, vmax=m.vmax)
+    with mm.AcousticVdEngine(g, m, mm.EngineOptions(ndamping=nd, free_surface=fs), dt) as e:
+        for s in range(12):
+            e.step(float(w[s]) * 1e6, src)
+            o.step(float(w[s]) * 1e6, src)
+        assert np.array_equal(e.pressure(), o.pressure())
+        for ax in range(3):
+            assert np.array_equal(e.velocity(ax), o.velocity(ax)), ax
