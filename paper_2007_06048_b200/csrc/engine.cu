@@ -88,11 +88,72 @@ struct mm_cd_engine {
     DevBuf<long long> rec_offs;
     DevBuf<float> traces;
     int nrec = 0, cap = 0;
-    DevBuf<int> counters;  // [0] step counter, [1] first bad step
+    DevBuf<int> counters;  // [0] step counter, [1] first bad step, [2] epilogue ticket
     TraceCopier tcopy;
     DevBuf<float> amps;
     long long steps = 0;
     std::unique_ptr<FastPlan> fast;
+    // Host-driven steps (mm_cd_step) in fast mode: the step's kernels (pass 1,
+    // boundary and interior over two streams) are captured once per buffer
+    // rotation state as a CUDA graph and replayed -- one launch instead of
+    // seven plus the cross-stream events; the injection (host amplitude) and
+    // the free surface follow it on the stream.  Keyed by `ic`, recaptured when
+    // (ip, in) differ from the capture or the CPML runs are rebuilt.
+    struct StepGraph {
+        cudaGraphExec_t exec = nullptr;
+        int ip = -1, in = -1;
+        long long launches = 0;
+    } step_graph[3];
+    bool fast_warm = false;  // one eager fast step ran (lazy work lists / dpsi_z built)
+    void drop_step_graphs() {
+        for (auto& g : step_graph) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            g = StepGraph{};
+        }
+    }
+    // Only where issuing the step's kernels one by one would bound the loop:
+    // eager issue costs ~65 us of host time per step, a replay ~20 us, but at
+    // 240^3 the eager step runs ~4 % faster on the device (147 vs 153 us,
+    // tools/e2e_probe.py), so grids past ~6 M points (a ~90 us step) issue
+    // eagerly.  MM_STEP_GRAPH=0/1 forces either.
+    bool step_graphs_enabled() const {
+        static const int forced = [] {
+            if (std::getenv("MM_NO_GRAPH") || std::getenv("MM_DEBUG_SYNC")) return 0;
+            const char* e = std::getenv("MM_STEP_GRAPH");
+            return e ? (e[0] == '1' ? 1 : 0) : -1;
+        }();
+        if (forced >= 0) return forced == 1;
+        return (double)lay.n[0] * lay.n[1] * lay.n[2] < 6.0e6;
+    }
+    void graph_fast_step(const StepParams& sp) {
+        StepGraph& g = step_graph[ic];
+        if (g.exec && (g.ip != ip || g.in != in)) {
+            cudaGraphExecDestroy(g.exec);
+            g = StepGraph{};
+        }
+        if (!g.exec) {
+            cudaGraph_t graph = nullptr;
+            const long long l0 = g_launches.load();
+            MM_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                fast->step(sp, -1LL, 0.0f, nullptr, nullptr, stream);
+            } catch (...) {
+                cudaStreamEndCapture(stream, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            MM_CUDA(cudaStreamEndCapture(stream, &graph));
+            g.launches = g_launches.load() - l0;
+            const cudaError_t err = cudaGraphInstantiate(&g.exec, graph, 0);
+            cudaGraphDestroy(graph);
+            MM_CUDA(err);
+            g.ip = ip;
+            g.in = in;
+            g_launches.fetch_sub(g.launches, std::memory_order_relaxed);  // counted per replay
+        }
+        MM_CUDA(cudaGraphLaunch(g.exec, stream));
+        note_launches(g.launches);
+    }
 
     StepParams params() const {
         StepParams s;
@@ -122,6 +183,8 @@ struct mm_cd_engine {
     // Local tables + the CPML memory runs (one per damping layer and axis,
     // allocated only where some a != 0) from prof.
     void setup_cpml() {
+        drop_step_graphs();  // captured with the previous runs' pointers
+        fast_warm = false;
         const long long nx4 = (lay.n[0] + 3) / 4 * 4;
         for (int ax = 0; ax < 3; ++ax) {
             const int n = lay.n[ax];
@@ -212,25 +275,41 @@ struct mm_cd_engine {
             fast->update_ranges(s, r, n, stream);
         }
     }
-    void finish_step(float amp, const int* src, const float* amp_dev, const int* step_dev) {
-        if (src) launch_inject(p[in].ptr, cv.ptr, src_off(src), amp, amp_dev, step_dev, stream);
-        if (free_surface && goff[2] == 0) launch_free_surface(p[in].ptr, lay, stream);
+    // One step: the update kernels, then k_epilogue (injection, free surface
+    // and -- from mm_cd_run -- the receiver sample and the step counter).
+    void full_step(float amp, const int* src, const float* amp_dev, int* step_dev,
+                   const RecParams* rec = nullptr) {
+        const StepParams sp = params();
+        const long long so = src ? src_off(src) : -1LL;
+        const bool fst = mode != MM_MODE_STRICT && fast;
+        if (fst) {
+            if (!amp_dev && !step_dev && fast_warm && step_graphs_enabled()) {
+                graph_fast_step(sp);
+            } else {
+                fast->step(sp, -1LL, 0.0f, nullptr, nullptr, stream);
+                fast_warm = true;
+            }
+        } else {
+            pass1();
+            update(0, 0, lay.n[2]);
+        }
+        Epilogue ep;
+        std::memset(&ep, 0, sizeof ep);
+        ep.p = sp.pn;
+        ep.cv = sp.cv;
+        ep.src_off = so;
+        ep.amp = amp;
+        ep.amp_dev = amp_dev;
+        ep.step_dev = step_dev;
+        ep.count = step_dev != nullptr;
+        ep.fs = free_surface && goff[2] == 0;
+        ep.lay = lay;
+        if (rec) ep.rec = *rec;
+        ep.done = counters.ptr + 2;
+        launch_epilogue(ep, stream);
         rotate();
         ++steps;
-    }
-    void full_step(float amp, const int* src, const float* amp_dev, const int* step_dev) {
-        if (mode != MM_MODE_STRICT && fast) {
-            fast->step(params(), src ? src_off(src) : -1LL, amp, amp_dev, step_dev, stream);
-            if (free_surface && goff[2] == 0) launch_free_surface(p[in].ptr, lay, stream);
-            rotate();
-            ++steps;
-            debug_sync("fast");
-            return;
-        }
-        pass1();
-        update(0, 0, lay.n[2]);
-        finish_step(amp, src, amp_dev, step_dev);
-        debug_sync("strict");
+        debug_sync(fst ? "fast" : "strict");
     }
     // MM_DEBUG_SYNC=all|fast|strict: synchronize after every step and name the engine whose
     // step faulted (diagnostics only)
@@ -263,6 +342,7 @@ struct mm_cd_engine {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
         }
+        drop_step_graphs();
         fast.reset();
         if (stream) cudaStreamDestroy(stream);
     }
@@ -462,7 +542,7 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     e->from_host(vp.data(), e->vp.ptr);
     launch_velocity_coeff(e->vp.ptr, e->cv.ptr, e->dt2, L.total, e->stream);
     e->setup_cpml();
-    e->counters.alloc_zero(2, e->stream);
+    e->counters.alloc_zero(3, e->stream);  // + the epilogue's block ticket
     if (mode == MM_MODE_FAST) {
         float* const bufs[3] = {e->p[0].ptr, e->p[1].ptr, e->p[2].ptr};
         e->fast = make_fast_plan(e->lay, device, bufs, e->cv.ptr);
@@ -749,13 +829,9 @@ int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src, in
     MM_CUDA(cudaEventCreate(&t1));
     MM_CUDA(cudaEventRecord(t0, e->stream));
     auto one_step = [&] {
-        e->full_step(0.0f, src, e->amps.ptr, step_dev);
-        if (record && e->nrec > 0) {
-            RecParams rp{e->p[e->ic].ptr, e->rec_offs.ptr,
-                         e->traces.ptr + (size_t)first_sample * e->nrec, e->nrec, 0, bad};
-            launch_record(rp, step_dev, e->stream);
-        }
-        launch_step_counter(step_dev, e->stream);
+        const RecParams rp{nullptr, e->rec_offs.ptr,
+                           e->traces.ptr + (size_t)first_sample * e->nrec, e->nrec, 0, bad};
+        e->full_step(0.0f, src, e->amps.ptr, step_dev, record && e->nrec > 0 ? &rp : nullptr);
     };
     // The first step runs eagerly (it also builds the lazily created work
     // lists); then the buffer rotation's period of three steps is captured

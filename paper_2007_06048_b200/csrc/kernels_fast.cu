@@ -325,23 +325,30 @@ public:
         const int imode = fc && zmode_ != 0 ? kFull : kInnerOnly;
         // (the Z-slab planes read dpsi_z from pass 1: no overlap then)
         const bool ov = overlap_ && imode == kInnerOnly;
-        if (ov) {
+        static const int inner_late = [] {
+            const char* e = std::getenv("MM_INNER_LATE");
+            return e ? std::atoi(e) : 0;
+        }();
+        auto fork_inner = [&] {
             // the interior kernel needs no CPML state: it runs on a second
             // stream beside pass 1 -> boundary and takes SMs as their tails free
             // them (a second branch of the captured graph)
-            MM_CUDA(cudaEventRecord(fork_, s));
             MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
             launch_inner(p, 0, lay_.n[2], imode, side_);
             MM_CUDA(cudaEventRecord(join_, side_));
-        }
+        };
+        if (ov) MM_CUDA(cudaEventRecord(fork_, s));  // the step's start
+        if (ov && inner_late == 0) fork_inner();
         dbg(s, "inner(side)", ov ? side_ : nullptr);
         launch_pass1(p, 0, lay_.n[2], s);
         dbg(s, "pass1", p1_side_);
+        if (ov && inner_late == 1) fork_inner();  // (issue order only: still from the start)
         if (fc)
             launch_boundary(p, 0, lay_.n[2], s);
         else
             strict_update(p, 2, 0, lay_.n[2], s);
         dbg(s, "boundary", nullptr);
+        if (ov && inner_late == 2) fork_inner();
         if (ov)
             MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
         else

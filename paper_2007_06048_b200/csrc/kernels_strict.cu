@@ -197,6 +197,51 @@ __global__ void k_record(RecParams rp, const int* step_dev) {
 
 __global__ void k_step_counter(int* step_dev) { *step_dev += 1; }
 
+// k_inject + k_free_surface + k_record + k_step_counter in one launch, with
+// the results of running them in that order.  Every thread reads the
+// pre-injection field; values that the injection or the surface change are
+// formed in registers (the injected source sample, 0 on the surface plane,
+// the odd mirror), and the one write of p_next[src] -- the only location
+// another thread could read -- is made by the last block to finish, after
+// all reads.  That block also advances the step counter.
+__global__ void k_epilogue(Epilogue e) {
+    const int step = e.step_dev ? *e.step_dev : e.rec.step;
+    const Layout& L = e.lay;
+    const bool has_src = e.src_off >= 0;
+    float inj = 0.0f;
+    if (has_src) {
+        const float a = e.amp_dev ? e.amp_dev[step] : e.amp;
+        inj = __fadd_rn(e.p[e.src_off], __fmul_rn(e.cv[e.src_off], a));  // propagator_impl.hpp:166-169
+    }
+    auto value = [&](long long o) { return has_src && o == e.src_off ? inj : e.p[o]; };
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int ex = L.n[0] + 2 * L.r;
+    const long long nfs = e.fs ? (long long)ex * L.ey : 0;
+    if (t < nfs) {  // cpml.hpp:103-111
+        const int i = (int)(t % ex) - L.r, j = (int)(t / ex) - L.r;
+        e.p[L.off(i, j, 0)] = 0.0f;
+        for (int m = 1; m <= L.r; ++m) e.p[L.off(i, j, -m)] = -value(L.off(i, j, m));
+    } else if (t - nfs < e.rec.nrec) {
+        const int r = (int)(t - nfs);
+        const long long o = e.rec.offs[r];
+        const bool on_surface = e.fs && o / L.plane == L.r;  // local z = 0
+        const float v = on_surface ? 0.0f : value(o);
+        e.rec.traces[(long long)step * e.rec.nrec + r] = v;
+        // ref: driver.cpp:68-71,108 check_finite(rec.at(0, n), n + 1)
+        if (r == 0 && !isfinite(v) && e.rec.bad_step) atomicMin(e.rec.bad_step, step + 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(e.done, 1) == gridDim.x - 1) {
+            __threadfence();
+            if (has_src && !(e.fs && e.src_off / L.plane == L.r)) e.p[e.src_off] = inj;
+            if (e.count) *e.step_dev = step + 1;
+            *e.done = 0;
+        }
+    }
+}
+
 // Host layout (i slowest, k fastest, ghosted) <-> device layout (k slowest,
 // i fastest, ghosted + padded), tiled 32x32 transposes over (i, k) per j.
 __global__ void k_to_device(const float* __restrict__ h, float* __restrict__ d, Layout lay) {
@@ -293,6 +338,16 @@ void launch_record(const RecParams& rp, const int* step_dev, cudaStream_t s) {
 
 void launch_step_counter(int* step_dev, cudaStream_t s) {
     k_step_counter<<<1, 1, 0, s>>>(step_dev);
+    note_launches(1);
+    MM_CUDA(cudaGetLastError());
+}
+
+void launch_epilogue(const Epilogue& ep, cudaStream_t s) {
+    const long long nfs = ep.fs ? (long long)(ep.lay.n[0] + 2 * ep.lay.r) * ep.lay.ey : 0;
+    const long long work = nfs + ep.rec.nrec;
+    if (work == 0 && ep.src_off < 0 && !ep.count) return;
+    const int blocks = (int)std::max<long long>((work + 255) / 256, 1);
+    k_epilogue<<<blocks, 256, 0, s>>>(ep);
     note_launches(1);
     MM_CUDA(cudaGetLastError());
 }

@@ -217,6 +217,22 @@ struct RecParams {
     int* bad_step;  // first 1-based step with non-finite receiver 0 (INT_MAX if none)
 };
 
+// The end of a step in one launch: source injection, free surface, receiver
+// sampling of the new field and the device step counter (k_epilogue).
+struct Epilogue {
+    float* p;              // p_next (p_cur after the rotation)
+    const float* cv;
+    long long src_off;     // < 0: no source
+    float amp;
+    const float* amp_dev;  // non-null: amplitude amp_dev[*step_dev]
+    int* step_dev;         // device step counter (or null: rec.step)
+    bool count;            // advance *step_dev once every block has read it
+    bool fs;               // free surface at local z = 0
+    Layout lay;
+    RecParams rec;         // nrec = 0: no sampling (rec.p is ignored: p)
+    int* done;             // block ticket (zero between launches)
+};
+
 // ---- launchers (kernels_strict.cu)
 void strict_pass1(const StepParams& p, int z_lo, int z_hi, cudaStream_t s);
 // region: 0 = every point, 1 = inner box only, 2 = damping slabs only
@@ -226,6 +242,7 @@ void launch_inject(float* pn, const float* cv, long long off, float amp, const f
 void launch_free_surface(float* p, const Layout& lay, cudaStream_t s);
 void launch_record(const RecParams& rp, const int* step_dev, cudaStream_t s);
 void launch_step_counter(int* step_dev, cudaStream_t s);
+void launch_epilogue(const Epilogue& ep, cudaStream_t s);
 void launch_to_device_layout(const float* host_layout, float* dev_layout, const Layout& lay,
                              cudaStream_t s);
 void launch_to_host_layout(const float* dev_layout, float* host_layout, const Layout& lay,

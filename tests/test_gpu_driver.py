@@ -112,3 +112,43 @@ def test_cli_model_shot_record_matches_reference(mm, tmp_path, oracle_ref):
     ref = oracle_ref.run(n, vp, nsteps=nsteps, nthreads=8)
     assert rec.dt == ref["dt"] and rec.nsteps == nsteps
     assert np.array_equal(rec.traces, ref["traces"])
+
+
+@pytest.mark.parametrize("mode", ["fast", "strict"])
+@pytest.mark.parametrize("src_z", [0, 2, 9])
+def test_step_epilogue_edge_placements(mm, oracle_port, mode, src_z):
+    """k_epilogue forms injection, free surface and receiver sampling in one
+    launch: a receiver on the source point, receivers on the surface plane and
+    within R of it, a source on the surface (zeroed by it) and within R of it
+    (mirrored) -- run() and step()+record() both equal the oracle's
+    inject -> free surface -> record order (propagator_impl.hpp:166-172,
+    source.cpp:61-66)."""
+    n, nd, steps = (26, 22, 24), (5, 4, 6), 14
+    h = (20.0, 20.0, 20.0)
+    grid = mm.make_grid(n, h)
+    m = mm.random_model(grid, seed=11)
+    dt = 1e-3
+    w = mm.ricker(25.0, dt, steps).samples * 1e3
+    src = (13, 11, src_z)
+    rec = np.array([src, (13, 11, 0), (12, 11, 0), (13, 11, 1), (13, 11, 3), (0, 0, 0),
+                    (25, 21, 23), (14, 11, src_z)])
+    ref = oracle_port.engine(n, m.vp, d=h, ndamping=nd, free_surface=True, taper=True, dt=dt,
+                             vmax=m.vmax)
+    want = np.zeros((len(rec), steps), np.float32)
+    for s in range(steps):
+        ref.step(float(w[s]), src)
+        p = ref.pressure().reshape(grid.shape)
+        want[:, s] = [p[i + 4, j + 4, k + 4] for i, j, k in rec]
+    assert (np.abs(want).max() > 0) == (src_z != 0)  # a source on the surface is zeroed
+    opts = mm.EngineOptions(ndamping=nd, taper=True, free_surface=True)
+    for use_loop in (False, True):
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, dt, m.vmax, mode=mode)
+        e.set_receivers(rec, steps)
+        if use_loop:
+            e.run(w, src)
+        else:
+            for s in range(steps):
+                e.step(float(w[s]), src)
+                e.record(s)
+        assert np.array_equal(e.pressure(), ref.pressure().reshape(grid.shape)), use_loop
+        assert np.array_equal(e.traces(), want), use_loop
