@@ -111,7 +111,8 @@ struct mm_cd_engine {
             g = StepGraph{};
         }
     }
-    // Only where issuing the step's kernels one by one would bound the loop:
+    // Per-step graphs (and mm_cd_run's rotation-period graph) only where
+    // issuing the step's kernels one by one would bound the loop:
     // eager issue costs ~65 us of host time per step, a replay ~20 us, but at
     // 240^3 the eager step runs ~4 % faster on the device (147 vs 153 us,
     // tools/e2e_probe.py), so grids past ~6 M points (a ~90 us step) issue
@@ -842,7 +843,9 @@ int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src, in
         one_step();
         ++s;
     }
-    const bool use_graph = nsteps - s >= 6 && std::getenv("MM_NO_GRAPH") == nullptr;
+    // (large grids issue eagerly: the host stays ahead, and the eager step is
+    // the faster one on the device -- see step_graphs_enabled)
+    const bool use_graph = nsteps - s >= 6 && e->step_graphs_enabled();
     if (use_graph) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;

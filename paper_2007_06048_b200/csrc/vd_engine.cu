@@ -341,7 +341,7 @@ struct mm_vd_engine {
     DevBuf<long long> rec_offs;
     DevBuf<float> traces;
     int nrec = 0, cap = 0;
-    DevBuf<int> counters;  // [0] step counter, [1] first bad step
+    DevBuf<int> counters;  // [0] step counter, [1] first bad step, [2] epilogue ticket
     TraceCopier tcopy;
     DevBuf<float> amps;
     long long steps = 0;
@@ -455,11 +455,27 @@ struct mm_vd_engine {
     void inject(float amp, const int* src, const float* amp_dev, const int* step_dev) {
         launch_inject(p.ptr, dtb.ptr, src_off(src), amp, amp_dev, step_dev, stream);
     }
-    void full_step(float amp, const int* src, const float* amp_dev, const int* step_dev) {
+    // velocity, pressure, then k_epilogue: injection, free surface and -- from
+    // mm_vd_run -- the receiver sample and the step counter in one launch
+    void full_step(float amp, const int* src, const float* amp_dev, int* step_dev,
+                   const RecParams* rec = nullptr) {
+        const long long so = src ? src_off(src) : -1LL;
         velocity();
         pressure();
-        if (src) inject(amp, src, amp_dev, step_dev);
-        if (free_surface) launch_free_surface(p.ptr, lay, stream);
+        Epilogue ep;
+        std::memset(&ep, 0, sizeof ep);
+        ep.p = p.ptr;
+        ep.cv = dtb.ptr;
+        ep.src_off = so;
+        ep.amp = amp;
+        ep.amp_dev = amp_dev;
+        ep.step_dev = step_dev;
+        ep.count = step_dev != nullptr;
+        ep.fs = free_surface;
+        ep.lay = lay;
+        if (rec) ep.rec = *rec;
+        ep.done = counters.ptr + 2;
+        launch_epilogue(ep, stream);
         ++steps;
     }
 
@@ -604,7 +620,7 @@ int mm_vd_create(const mm_grid* grid, const float* vp, const float* rho,
     e->from_host(irh.data(), e->ir.ptr);
     e->from_host(dtbh.data(), e->dtb.ptr);
     e->setup_cpml();
-    e->counters.alloc_zero(2, e->stream);
+    e->counters.alloc_zero(3, e->stream);  // + the epilogue's block ticket
     if (const char* zc = std::getenv("MM_VD_ZC")) e->zc = std::max(1, std::atoi(zc));
     if (!std::getenv("MM_VD_SIMPLE")) {
         float* const vv[3] = {e->v[0].ptr, e->v[1].ptr, e->v[2].ptr};
@@ -810,13 +826,9 @@ int mm_vd_run(mm_vd_engine* e, const float* amps, int nsteps, const int* src, in
     MM_CUDA(cudaEventCreate(&t1));
     MM_CUDA(cudaEventRecord(t0, e->stream));
     auto one_step = [&] {
-        e->full_step(0.0f, src, e->amps.ptr, step_dev);
-        if (record && e->nrec > 0) {
-            RecParams rp{e->p.ptr, e->rec_offs.ptr, e->traces.ptr + (size_t)first_sample * e->nrec,
-                         e->nrec, 0, bad};
-            launch_record(rp, step_dev, e->stream);
-        }
-        launch_step_counter(step_dev, e->stream);
+        const RecParams rp{nullptr, e->rec_offs.ptr,
+                           e->traces.ptr + (size_t)first_sample * e->nrec, e->nrec, 0, bad};
+        e->full_step(0.0f, src, e->amps.ptr, step_dev, record && e->nrec > 0 ? &rp : nullptr);
     };
     // The fields update in place, so one step is captured as a CUDA graph and
     // replayed; per-step values come through the device step counter.
