@@ -33,6 +33,13 @@ std::atomic<long long> g_launches{0};
 
 void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launches_so_far() { return g_launches.load(); }
+int main_stream_priority() {
+    static const int v = [] {
+        const char* e = std::getenv("MM_MAIN_PRIO");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
 
 int set_api_error(int code, const std::string& msg, int step) {
     g_err = msg;
@@ -497,7 +504,16 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     auto e = std::make_unique<mm_cd_engine>();
     e->device = device;
     e->mode = mode;
-    MM_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    // MM_MAIN_PRIO=1|2 (experiment): the step's stream (pass 1 z runs ->
+    // boundary, the critical path) at the greatest priority, above the
+    // interior kernel's side stream
+    if (main_stream_priority() > 0) {
+        int lo = 0, hi = 0;
+        MM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        MM_CUDA(cudaStreamCreateWithPriority(&e->stream, cudaStreamNonBlocking, hi));
+    } else {
+        MM_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    }
     e->lay = Layout::make(local->n, local->radius);
     e->hg = HostGrid{{local->n[0], local->n[1], local->n[2]}, local->radius};
     for (int a = 0; a < 3; ++a) {

@@ -223,8 +223,8 @@ public:
         // stream, the critical path) are scheduled first
         int prio_lo = 0, prio_hi = 0;
         MM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        MM_CUDA(cudaStreamCreateWithPriority(&p1_side_, cudaStreamNonBlocking, prio_lo));
-        (void)prio_hi;
+        MM_CUDA(cudaStreamCreateWithPriority(&p1_side_, cudaStreamNonBlocking,
+                                             main_stream_priority() >= 2 ? prio_hi : prio_lo));
         { const char* e = std::getenv("MM_PDL"); pdl_ = !e || e[0] != '0'; }
         MM_CUDA(cudaEventCreateWithFlags(&p1_fork_, cudaEventDisableTiming));
         MM_CUDA(cudaEventCreateWithFlags(&p1_join_, cudaEventDisableTiming));

@@ -37,6 +37,7 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 
 // Counts kernel launches issued through the library (evidence for bench.py).
 void note_launches(long long n);
+int main_stream_priority();  // MM_MAIN_PRIO (engine.cu)
 long long launches_so_far();
 
 // C-ABI error plumbing (engine.cu): records the thread-local message/step

@@ -293,3 +293,37 @@ def test_vd_tiny_and_degenerate_grids(mm, oracle_port, n, r, nd, fs):
         assert np.array_equal(e.pressure(), o.pressure())
         for ax in range(3):
             assert np.array_equal(e.velocity(ax), o.velocity(ax)), ax
+
+
+@pytest.mark.parametrize("src_z", [0, 2, 9])
+def test_vd_step_epilogue_edge_placements(mm, oracle_port, src_z):
+    """acoustic_iso's k_epilogue (injection, free surface, receiver sample in
+    one launch): receivers on the source point, on and near the surface, a
+    source on the surface and within R of it; run() and step()+record() both
+    equal the oracle's inject -> free surface -> record order."""
+    n, nd, steps, dt = (26, 22, 24), (5, 4, 6), 12, 5e-4
+    g, m = _model(mm, n, 4, seed=7)
+    w = mm.integrate_wavelet(mm.ricker(25.0, dt, steps)).samples * 1e6
+    src = (13, 11, src_z)
+    rec = np.array([src, (13, 11, 0), (12, 11, 0), (13, 11, 1), (13, 11, 3), (0, 0, 0),
+                    (25, 21, 23), (14, 11, src_z)])
+    o = oracle_port.vd_engine(n, m.vp, m.rho, radius=4, ndamping=nd, free_surface=True, dt=dt,
+                              vmax=m.vmax)
+    want = np.zeros((len(rec), steps), np.float32)
+    for s in range(steps):
+        o.step(float(w[s]), src)
+        p = np.asarray(o.pressure()).reshape(g.shape)
+        want[:, s] = [p[i + 4, j + 4, k + 4] for i, j, k in rec]
+    assert (np.abs(want).max() > 0) == (src_z != 0)  # a source on the surface is zeroed
+    opts = mm.EngineOptions(ndamping=nd, free_surface=True)
+    for use_loop in (False, True):
+        with mm.AcousticVdEngine(g, m, opts, dt) as e:
+            e.set_receivers(rec, steps)
+            if use_loop:
+                e.run(w, src)
+            else:
+                for s in range(steps):
+                    e.step(float(w[s]), src)
+                    e.record(s)
+            assert np.array_equal(e.pressure(), o.pressure()), use_loop
+            assert np.array_equal(e.traces(), want), use_loop
