@@ -38,9 +38,13 @@ import subprocess
 import sys
 import threading
 import time
+
 from pathlib import Path
 
 import numpy as np
+
+# before any CUDA context exists (see paper_2007_06048_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -267,6 +271,8 @@ def run_ours(args):
     wall = time.perf_counter() - wall0
     e2e_ms = max(e0.elapsed_time(e1), wall * 1e3)
     e2e = pts * args.steps / (e2e_ms * 1e-3) / 1e9
+    print(f"e2e: device {e0.elapsed_time(e1):.2f} ms, wall {wall * 1e3:.2f} ms over {args.steps} "
+          f"steps", file=sys.stderr)
 
     peak, peak_src = measured_peak()
     kb = kernel_bytes(n, nd)

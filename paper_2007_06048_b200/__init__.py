@@ -6,6 +6,15 @@ Python front-end over the C-ABI CUDA library ``libminimod_b200.so``
 ``ricker``, ``default_layered_model`` ...; plus the next
 propagator, ``AcousticVdEngine`` (acoustic_iso, variable density).
 """
+import os as _os
+
+# Each engine drives four CUDA streams (step, pass-1 side, interior side, trace
+# copies).  With the driver's default of 8 hardware connections, a third engine
+# in a process shares queues with the others and its interior kernel
+# serialises behind pass 1 (168 vs 153 us/step at 240^3).  Only effective when
+# set before the process creates its CUDA context.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from ._lib import (CollectiveError, ConfigError, CudaError, InstabilityError, MinimodError,
                    ValidationError, device_count, kernel_launch_count)
 from .driver import (RunReport, SimConfig, build_geometry, cfl_dt, render_parameter_block,
