@@ -16,6 +16,7 @@ b bench_vd_512 --propagator acoustic_iso --grid 512 --steps 100
 b bench_vd_1000 --propagator acoustic_iso --grid 1000 --steps 20 --warmup 3
 b bench_reference_240 --impl reference --steps 20 --warmup 3
 b bench_vd_reference_240 --impl reference --propagator acoustic_iso --steps 20 --warmup 3
+[ "${1:-}" = "--no-ncu" ] && exit 0
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/launches_240.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
 echo "launch list rc=$?"
