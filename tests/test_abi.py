@@ -1,6 +1,9 @@
 """The C-ABI library loads and exports every symbol include/minimod_b200.h
 declares; error codes map to the reference's exception types.  CPU only."""
+import os
 import re
+import subprocess
+import sys
 from pathlib import Path
 
 import pytest
@@ -63,3 +66,22 @@ def test_error_mapping_without_gpu(mm):
     with pytest.raises(ValueError):
         from paper_2007_06048_b200 import _lib
         _lib.check(_lib.lib().mm_cd_step(None, 0.0, None))
+
+
+def _env_after_import(env):
+    code = (f"import os, sys; sys.path.insert(0, {str(ROOT)!r}); import paper_2007_06048_b200;"
+            "print(os.environ['CUDA_DEVICE_MAX_CONNECTIONS'])")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=300)
+    return out.stdout.strip(), out.stderr[-500:]
+
+
+def test_package_raises_hardware_queue_default():
+    """Importing the package asks for 32 CUDA hardware connections unless the
+    user chose a value (several engines per process otherwise share queues and
+    serialise their side streams)."""
+    env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
+    got, err = _env_after_import(env)
+    assert got == "32", err
+    got, err = _env_after_import({**env, "CUDA_DEVICE_MAX_CONNECTIONS": "4"})
+    assert got == "4", err
