@@ -26,6 +26,11 @@
 namespace mmb {
 
 namespace {
+// Every engine drives four streams; with the driver's default of 8 hardware
+// connections a third engine in a process shares queues with the others and
+// its interior kernel serialises behind pass 1.  Ask for 32 at load time,
+// unless the host chose a value (effective only before the CUDA context).
+const int g_connections = [] { return setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }();
 thread_local std::string g_err;
 thread_local int g_step = 0;
 std::atomic<long long> g_launches{0};
