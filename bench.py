@@ -86,9 +86,14 @@ def byte_model(n, nd, r=4):
     return 16.0 * N + 16.0 * damped, N, damped
 
 
-def kernel_bytes(n, nd, r=4):
-    """Algorithmic bytes per launch of the three step kernels:
+def kernel_bytes(n, nd, r=4, nrec=0):
+    """Algorithmic bytes per launch of the step kernels:
+      cpml     16 B per slab point (p_cur, p_prev, c read; p_next write) + 16 B
+               per damped-axis point (psi and zeta read + write): the fused
+               one-pass CPML kernel, exactly the byte model's damping share
       inner    16 B per inner-box point (p_cur, p_prev, c read; p_next write)
+      epilogue 12 B per receiver (offset read, sample read + write)
+    and of the two-pass path (layouts k_cpml does not serve):
       boundary 16 B per slab point + 12 B per damped-axis point (psi or dpsi_z
                read, zeta read + write)
       pass1    8 B per damped-axis point (psi read + write) + 4 B per slab
@@ -99,7 +104,9 @@ def kernel_bytes(n, nd, r=4):
     inner = float(np.prod([n[a] - 2 * nd[a] for a in range(3)]))
     slab = N - inner
     dpz = 2.0 * (nd[2] + 2 * r) * n[0] * n[1] if nd[2] > 0 else 0.0
-    return {"inner": 16.0 * inner, "boundary": 16.0 * slab + 12.0 * damped,
+    return {"cpml": 16.0 * slab + 16.0 * damped, "inner": 16.0 * inner,
+            "epilogue": 12.0 * nrec,
+            "boundary": 16.0 * slab + 12.0 * damped,
             "pass1": 8.0 * damped + 4.0 * slab + 4.0 * dpz}
 
 
@@ -193,6 +200,7 @@ def run_ours(args):
                               device=local, mode=args.mode)
     geo = mm.default_receivers(grid, nd)
     eng.set_receivers(geo.receivers, total)
+    nrec = geo.nreceivers()
     ext = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
 
     # clock ramp (untimed): a throw-away engine steps for >= 0.3 s so the SM
@@ -226,31 +234,21 @@ def run_ours(args):
     pts = float(n[0]) * n[1] * n[2]
     value = pts * args.steps / (ms * 1e-3) / 1e9
 
-    # per-kernel durations over K steps, in the step's own order (pass 1,
-    # boundary, interior), CUDA events on the engine's stream
-    k_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    for s in range(args.steps):
-        ev = k_ev[s]
-        ev[0].record(ext)
-        eng.update_boundary_psi()
-        ev[1].record(ext)
-        eng.update_boundary()
-        ev[2].record(ext)
-        eng.update_inner()
-        ev[3].record(ext)
-        eng.inject_source(float(w[s % total]), src)
-        eng.rotate()
-        ev[4].record(ext)
+    # per-kernel durations inside the real step (the CPML and interior kernels
+    # concurrent on their two streams): K more steps of the same device loop,
+    # every kernel bracketed by CUDA events on the stream it is launched on
+    eng.kernel_timing(True)
+    eng.run(w[args.warmup:total], src, record=False)
+    kt = eng.kernel_times()
+    eng.kernel_timing(False)
     torch.cuda.synchronize()
-    kms = {k: statistics.mean(e[i].elapsed_time(e[i + 1]) for e in k_ev)
-           for i, k in enumerate(("pass1", "boundary", "inner"))}
-
+    kms = {k: v[0] / v[1] for k, v in kt.items() if v[1] > 0}
+    klaunch = {k: int(v[1]) for k, v in kt.items()}
     # e2e through the public API with host buffers
     eng2 = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp,
                                mm.EngineOptions(ndamping=nd, taper=True), dt, model.vmax,
                                device=local, mode=args.mode)
     eng2.set_receivers(geo.receivers, total)
-    nrec = geo.nreceivers()
     host_out = torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
     for s in range(args.warmup):
         eng2.step(float(w[s]), src)
@@ -275,14 +273,16 @@ def run_ours(args):
           f"steps", file=sys.stderr)
 
     peak, peak_src = measured_peak()
-    kb = kernel_bytes(n, nd)
+    kb = kernel_bytes(n, nd, r, nrec)
     dominant = max(kms, key=kms.get)
     achieved = kb[dominant] / (kms[dominant] * 1e-3) / 1e9
     step_bytes, _, _ = byte_model(n, nd)
     step_gbs = step_bytes * args.steps / (ms * 1e-3) / 1e9
     traffic = ncu_traffic(f"{edge}^3", dominant)
-    per_kernel = {k: {"ms": round(kms[k], 4), "algorithmic_bytes": kb[k],
-                      "achieved_gbs": round(kb[k] / (kms[k] * 1e-3) / 1e9, 1)} for k in kms}
+    per_kernel = {k: {"ms": round(kms[k], 4), "launches": klaunch[k],
+                      "algorithmic_bytes": kb.get(k),
+                      "achieved_gbs": (round(kb[k] / (kms[k] * 1e-3) / 1e9, 1)
+                                       if k in kb else None)} for k in kms}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
@@ -292,6 +292,7 @@ def run_ours(args):
         "config": {"workload": f"acoustic_iso_cd r={r} {edge}^3 grid, nd=27 CPML, taper, "
                                f"{nrec} surface receivers (BASELINE configs[1])",
                    "grid": list(n), "radius": r, "ndamping": list(nd), "mode": args.mode,
+                   "cpml_path": eng.cpml_path(),
                    "l2": "working set (3 p fields + c + CPML) > 126 MB L2; no flush"},
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": 4,
                 "d2h_bytes_per_step": 4 * nrec},

@@ -42,11 +42,14 @@ typedef enum mm_status {
     MM_ENCCL = 6         /* collective failure (multi-GPU plumbing) */
 } mm_status;
 
-/* Arithmetic modes of the device step.
- *  MM_MODE_STRICT: reference association order, no FMA contraction;
- *                  bit-identical to the CPU reference.
- *  MM_MODE_FAST:   the TMA/register-queue kernels (default). */
-typedef enum mm_mode { MM_MODE_FAST = 0, MM_MODE_STRICT = 1 } mm_mode;
+/* Kernel families / arithmetic of the device step (chosen at create time).
+ *  MM_MODE_FAST:     the TMA / register-queue kernels (default), reference
+ *                    association order with every operation separately
+ *                    rounded: bit-identical to the CPU reference.
+ *  MM_MODE_STRICT:   one thread per point, same arithmetic; bit-identical.
+ *  MM_MODE_FAST_FMA: the fast kernels with FMA contraction of the reference
+ *                    order (not bit-identical; ~1e-5 relative). */
+typedef enum mm_mode { MM_MODE_FAST = 0, MM_MODE_STRICT = 1, MM_MODE_FAST_FMA = 2 } mm_mode;
 
 /* ref: grid.hpp:49-73 Grid3D (n, d, radius; stagger is not used by CD). */
 typedef struct mm_grid {
@@ -75,6 +78,13 @@ const char* mm_version(void);
 int mm_device_count(int* count);
 /* Kernel launches issued by this process so far (all engines). */
 long long mm_kernel_launch_count(void);
+/* Process-wide tuning parameters (work-item sizes, CUDA-graph use, kernel
+ * families, diagnostics; the list and defaults are in csrc/engine.cu
+ * kTunables).  The library never reads the environment; most parameters are
+ * read when an engine is created.  Unknown names: MM_EINVAL. */
+int mm_set_tuning(const char* name, long long value);
+int mm_get_tuning(const char* name, long long* value);
+int mm_reset_tuning(void);
 
 /* ------------------------------------------------------------------------
  * Host numerics (C++; bit-identical to the reference)
@@ -183,6 +193,20 @@ int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src_loc
  * The halo transport itself (NCCL send/recv) is issued by the host runtime
  * on the engine's stream; these expose the contiguous plane ranges.
  * --------------------------------------------------------------------- */
+/* Which kernels update the damping slabs in a full step: "cpml" (the fused
+ * one-pass kernel), "two-pass" (CPML pass 1 then pass 2) or "strict". */
+int mm_cd_cpml_path(mm_cd_engine* e, char* buf, int cap);
+/* Per-kernel device timing of fast-mode steps (benchmark evidence): on != 0
+ * brackets every kernel a step launches with CUDA events on the stream it is
+ * launched on (steps then issue eagerly, no CUDA graphs).  Enabling or
+ * disabling clears the totals. */
+int mm_cd_kernel_timing(mm_cd_engine* e, int on);
+/* Totals since timing was enabled, one entry per kernel name: names[i]
+ * (NUL-terminated), total_ms[i], launches[i] for i < min(cap, *n); *n = the
+ * number of kernel names.  Any output array may be NULL. */
+int mm_cd_kernel_times(mm_cd_engine* e, int cap, char (*names)[32], double* total_ms,
+                       long long* launches, int* n);
+
 /* CUDA stream (cudaStream_t) the engine launches on. */
 int mm_cd_stream(mm_cd_engine* e, void** stream);
 /* Device pointer + byte size of the r z-planes of p_cur on one side:

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / (
     else "libminimod_b200.so")
 
 MM_OK, MM_ECONFIG, MM_EVALIDATION, MM_EINSTABILITY, MM_EINVAL, MM_ECUDA, MM_ENCCL = range(7)
-MM_MODE_FAST, MM_MODE_STRICT = 0, 1
+MM_MODE_FAST, MM_MODE_STRICT, MM_MODE_FAST_FMA = 0, 1, 2
 
 
 class MinimodError(RuntimeError):
@@ -90,6 +90,9 @@ SIGNATURES = {
     "mm_version": [],
     "mm_device_count": [_ip],
     "mm_kernel_launch_count": [],
+    "mm_set_tuning": [C.c_char_p, C.c_longlong],
+    "mm_get_tuning": [C.c_char_p, C.POINTER(C.c_longlong)],
+    "mm_reset_tuning": [],
     "mm_second_derivative_coeffs": [C.c_int, C.c_double, _dp, _dp],
     "mm_central_first_derivative_coeffs": [C.c_int, C.c_double, _dp],
     "mm_cfl_dt": [C.c_double, C.POINTER(mm_grid), C.c_double, _dp],
@@ -127,6 +130,9 @@ SIGNATURES = {
     "mm_cd_copy_trace_step": [_P, C.c_int, _fp, C.c_int],
     "mm_cd_run": [_P, _fp, C.c_int, _ip, C.c_int, C.c_int, _fp],
     "mm_cd_stream": [_P, C.POINTER(_P)],
+    "mm_cd_kernel_timing": [_P, C.c_int],
+    "mm_cd_cpml_path": [_P, C.c_char_p, C.c_int],
+    "mm_cd_kernel_times": [_P, C.c_int, C.c_void_p, _dp, C.POINTER(C.c_longlong), _ip],
     "mm_cd_halo_planes": [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_size_t)],
     "mm_cd_next_halo_planes": [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_size_t)],
     "mm_cd_update_planes": [_P, C.c_int, C.c_int],
@@ -211,6 +217,39 @@ def device_count() -> int:
     n = C.c_int()
     check(lib().mm_device_count(C.byref(n)))
     return n.value
+
+
+def set_tuning(name: str, value: int) -> None:
+    """Process-wide tuning parameter (mm_set_tuning; csrc/engine.cu kTunables)."""
+    check(lib().mm_set_tuning(name.encode(), int(value)))
+
+
+def get_tuning(name: str) -> int:
+    v = C.c_longlong()
+    check(lib().mm_get_tuning(name.encode(), C.byref(v)))
+    return v.value
+
+
+def reset_tuning() -> None:
+    check(lib().mm_reset_tuning())
+
+
+class tuned:
+    """Context manager: tuning parameters set for the block, then restored."""
+
+    def __init__(self, **params):
+        self.params = params
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.params.items():
+            self.saved[k] = get_tuning(k)
+            set_tuning(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            set_tuning(k, v)
 
 
 def kernel_launch_count() -> int:

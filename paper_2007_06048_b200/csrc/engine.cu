@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -26,25 +27,106 @@
 namespace mmb {
 
 namespace {
-// Every engine drives four streams; with the driver's default of 8 hardware
-// connections a third engine in a process shares queues with the others and
-// its interior kernel serialises behind pass 1.  Ask for 32 at load time,
-// unless the host chose a value (effective only before the CUDA context).
-const int g_connections = [] { return setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }();
 thread_local std::string g_err;
 thread_local int g_step = 0;
 std::atomic<long long> g_launches{0};
+
+// Tuning parameters: name, product default, meaning.  Changed only through
+// mm_set_tuning (no environment reads in the library).
+struct Tunable {
+    const char* name;
+    long long def;
+};
+const Tunable kTunables[] = {
+    {"step_graph", -1},  // host-driven steps as CUDA graphs: -1 auto (grids < 6 M points), 0 off, 1 on
+    {"cpml_fused", 1},   // fast mode: one-pass CPML kernel k_cpml where the layout allows it (0: k_p1 + k_bnd)
+    {"cpml_zt", 0},      // k_cpml planes per work item (0: automatic)
+    {"overlap", 1},      // interior kernel on a side stream beside the CPML kernels
+    {"pdl", 1},          // programmatic dependent launch of k_bnd after k_p1
+    {"inner_late", 0},   // (experiment) issue the interior kernel after pass 1 (1) or the boundary (2)
+    {"main_prio", 0},    // (experiment) step stream at the greatest priority
+    {"debug_sync", 0},   // (diagnostics) synchronize after every kernel (1) or every step (2)
+    {"l2_promo", 2},     // TMA L2 promotion: 0 none, 1 64 B, 2 128 B, 3 256 B
+    {"inner_zt", 48},    // k_inner planes per work item (target)
+    {"bnd_zt", 12},      // k_bnd planes per work item (target)
+    {"p1_zt", 16},       // k_p1 planes per work item (target)
+    {"zslabs", -1},      // Z slabs: -1 auto, 0 k_bnd tiles, 1 k_zslab after k_inner, 2 k_zslab columns
+    {"bnd_kinds", 7},    // (profiling) slab kinds k_bnd updates (bit mask X/Y/Z)
+    {"bnd_ctas", 0},     // (diagnostics) cap on k_bnd CTAs (0: none)
+    {"p1_axes", 7},      // (profiling) run axes k_p1 updates (bit mask)
+    {"vd_zchunks", 0},   // acoustic_iso: z chunks per tile column (0: automatic)
+    {"vd_ctas", 0},      // acoustic_iso (diagnostics): cap on CTAs (0: none)
+    {"vd_zc", 0},        // acoustic_iso: simple-kernel z chunk (0: default)
+    {"vd_simple", 0},    // acoustic_iso: one-thread-per-point kernels instead of the TMA kernels
+};
+std::mutex g_tun_mu;
+std::map<std::string, long long> g_tun;
+
+const Tunable* find_tunable(const char* name) {
+    if (!name) return nullptr;
+    for (const auto& t : kTunables)
+        if (std::strcmp(t.name, name) == 0) return &t;
+    return nullptr;
+}
 }  // namespace
+
+long long tuning(const char* name) {
+    const Tunable* t = find_tunable(name);
+    if (!t) raise(ST_INVAL, std::string("unknown tuning parameter ") + (name ? name : "(null)"));
+    std::lock_guard<std::mutex> lk(g_tun_mu);
+    const auto it = g_tun.find(t->name);
+    return it == g_tun.end() ? t->def : it->second;
+}
+
+// ---- KernelTimer
+cudaEvent_t KernelTimer::get() {
+    if (!pool_.empty()) {
+        cudaEvent_t e = pool_.back();
+        pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    MM_CUDA(cudaEventCreate(&e));
+    return e;
+}
+int KernelTimer::begin(const char* name, cudaStream_t s) {
+    if (!on) return -1;
+    Rec r{name, get(), get()};
+    MM_CUDA(cudaEventRecord(r.a, s));
+    pending_.push_back(r);
+    return (int)pending_.size() - 1;
+}
+void KernelTimer::end(int idx, cudaStream_t s) {
+    if (idx < 0) return;
+    MM_CUDA(cudaEventRecord(pending_[idx].b, s));
+}
+void KernelTimer::collect() {
+    for (auto& r : pending_) {
+        MM_CUDA(cudaEventSynchronize(r.b));
+        float ms = 0;
+        MM_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        auto& a = acc[r.name];
+        a.first += ms;
+        a.second += 1;
+        pool_.push_back(r.a);
+        pool_.push_back(r.b);
+    }
+    pending_.clear();
+}
+void KernelTimer::reset() {
+    collect();
+    acc.clear();
+}
+KernelTimer::~KernelTimer() {
+    for (auto& r : pending_) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : pool_) cudaEventDestroy(e);
+}
 
 void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launches_so_far() { return g_launches.load(); }
-int main_stream_priority() {
-    static const int v = [] {
-        const char* e = std::getenv("MM_MAIN_PRIO");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
 
 int set_api_error(int code, const std::string& msg, int step) {
     g_err = msg;
@@ -129,12 +211,12 @@ struct mm_cd_engine {
     // 240^3 the eager step runs ~4 % faster on the device (147 vs 153 us,
     // tools/e2e_probe.py), so grids past ~6 M points (a ~90 us step) issue
     // eagerly.  MM_STEP_GRAPH=0/1 forces either.
+    // ("step_graph" tuning forces either; kernel timing and debug
+    // synchronisation need the eager path)
     bool step_graphs_enabled() const {
-        static const int forced = [] {
-            if (std::getenv("MM_NO_GRAPH") || std::getenv("MM_DEBUG_SYNC")) return 0;
-            const char* e = std::getenv("MM_STEP_GRAPH");
-            return e ? (e[0] == '1' ? 1 : 0) : -1;
-        }();
+        if (fast && fast->timer.on) return false;
+        if (tuning("debug_sync")) return false;
+        const long long forced = tuning("step_graph");
         if (forced >= 0) return forced == 1;
         return (double)lay.n[0] * lay.n[1] * lay.n[2] < 6.0e6;
     }
@@ -291,7 +373,7 @@ struct mm_cd_engine {
     // One step: the update kernels, then k_epilogue (injection, free surface
     // and -- from mm_cd_run -- the receiver sample and the step counter).
     void full_step(float amp, const int* src, const float* amp_dev, int* step_dev,
-                   const RecParams* rec = nullptr) {
+                   const RecParams* rec = nullptr, long long check_off = -1) {
         const StepParams sp = params();
         const long long so = src ? src_off(src) : -1LL;
         const bool fst = mode != MM_MODE_STRICT && fast;
@@ -306,6 +388,7 @@ struct mm_cd_engine {
             pass1();
             update(0, 0, lay.n[2]);
         }
+        const int te = fst ? fast->timer.begin("epilogue", stream) : -1;
         Epilogue ep;
         std::memset(&ep, 0, sizeof ep);
         ep.p = sp.pn;
@@ -318,33 +401,36 @@ struct mm_cd_engine {
         ep.fs = free_surface && goff[2] == 0;
         ep.lay = lay;
         if (rec) ep.rec = *rec;
+        ep.check_off = check_off;
         ep.done = counters.ptr + 2;
         launch_epilogue(ep, stream);
+        if (te >= 0) fast->timer.end(te, stream);
         rotate();
         ++steps;
         debug_sync(fst ? "fast" : "strict");
     }
-    // MM_DEBUG_SYNC=all|fast|strict: synchronize after every step and name the engine whose
-    // step faulted (diagnostics only)
+    // tuning "debug_sync" != 0: synchronize after every step and name the
+    // engine whose step faulted (diagnostics only)
     void debug_sync(const char* what) {
-        static const char* sel = std::getenv("MM_DEBUG_SYNC");
-        if (!sel || !(std::strcmp(sel, "all") == 0 || std::strcmp(sel, what) == 0)) return;
+        if (!tuning("debug_sync")) return;
         const cudaError_t e = cudaStreamSynchronize(stream);
         if (e != cudaSuccess)
             raise(ST_CUDA, std::string("fault in ") + what + " step " + std::to_string(steps) +
                                ": " + cudaGetErrorString(e));
     }
 
+    // host <-> device layout transposes go through one engine-lifetime
+    // staging buffer (allocated on first use), so pressure() costs a transpose
+    // and a copy, not an allocation
+    DevBuf<float> stage;
     void to_host(const float* dev, float* host) {
-        DevBuf<float> stage;
-        stage.alloc(hg.volume());
+        if (stage.count < hg.volume()) stage.alloc(hg.volume());
         launch_to_host_layout(dev, stage.ptr, lay, stream);
         MM_CUDA(cudaMemcpyAsync(host, stage.ptr, hg.volume() * sizeof(float),
                                 cudaMemcpyDeviceToHost, stream));
         MM_CUDA(cudaStreamSynchronize(stream));
     }
     void from_host(const float* host, float* dev) {
-        DevBuf<float> stage;
         stage.upload(host, hg.volume(), stream);
         launch_to_device_layout(stage.ptr, dev, lay, stream);
         MM_CUDA(cudaStreamSynchronize(stream));
@@ -373,6 +459,29 @@ void use(mm_cd_engine* e) {
 extern "C" {
 
 const char* mm_last_error(void) { return g_err.c_str(); }
+
+int mm_set_tuning(const char* name, long long value) {
+    MM_API_BEGIN
+    const Tunable* t = find_tunable(name);
+    if (!t) raise(ST_INVAL, std::string("unknown tuning parameter ") + (name ? name : "(null)"));
+    std::lock_guard<std::mutex> lk(g_tun_mu);
+    g_tun[t->name] = value;
+    MM_API_END
+}
+
+int mm_reset_tuning(void) {
+    MM_API_BEGIN
+    std::lock_guard<std::mutex> lk(g_tun_mu);
+    g_tun.clear();
+    MM_API_END
+}
+
+int mm_get_tuning(const char* name, long long* value) {
+    MM_API_BEGIN
+    need(value, "value");
+    *value = tuning(name);
+    MM_API_END
+}
 int mm_last_instability_step(void) { return g_step; }
 const char* mm_version(void) { return "minimod-b200 0.1 (sm_100a)"; }
 long long mm_kernel_launch_count(void) { return g_launches.load(); }
@@ -497,7 +606,8 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     }
     if (local->radius < 1 || local->radius > kMaxR)
         raise(ST_CONFIG, "stencil radius must be in [1, 8], got " + std::to_string(local->radius));
-    if (mode != MM_MODE_FAST && mode != MM_MODE_STRICT) raise(ST_INVAL, "unknown mode");
+    if (mode != MM_MODE_FAST && mode != MM_MODE_STRICT && mode != MM_MODE_FAST_FMA)
+        raise(ST_INVAL, "unknown mode");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -509,10 +619,9 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     auto e = std::make_unique<mm_cd_engine>();
     e->device = device;
     e->mode = mode;
-    // MM_MAIN_PRIO=1|2 (experiment): the step's stream (pass 1 z runs ->
-    // boundary, the critical path) at the greatest priority, above the
-    // interior kernel's side stream
-    if (main_stream_priority() > 0) {
+    // tuning "main_prio" (experiment): the step's stream at the greatest
+    // priority, above the interior kernel's side stream
+    if (tuning("main_prio") > 0) {
         int lo = 0, hi = 0;
         MM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         MM_CUDA(cudaStreamCreateWithPriority(&e->stream, cudaStreamNonBlocking, hi));
@@ -565,9 +674,11 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     launch_velocity_coeff(e->vp.ptr, e->cv.ptr, e->dt2, L.total, e->stream);
     e->setup_cpml();
     e->counters.alloc_zero(3, e->stream);  // + the epilogue's block ticket
-    if (mode == MM_MODE_FAST) {
+    if (mode != MM_MODE_STRICT) {
         float* const bufs[3] = {e->p[0].ptr, e->p[1].ptr, e->p[2].ptr};
-        e->fast = make_fast_plan(e->lay, device, bufs, e->cv.ptr);
+        // MM_MODE_FAST: reference order, every operation rounded (bit-exact);
+        // MM_MODE_FAST_FMA: reference order with FMA contraction
+        e->fast = make_fast_plan(e->lay, device, bufs, e->cv.ptr, mode == MM_MODE_FAST ? 2 : 1);
     }
     MM_CUDA(cudaStreamSynchronize(e->stream));
     *out = e.release();
@@ -846,14 +957,37 @@ int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src, in
                             e->stream));
     int* step_dev = e->counters.ptr;
     int* bad = e->counters.ptr + 1;
-    cudaEvent_t t0, t1;
-    MM_CUDA(cudaEventCreate(&t0));
-    MM_CUDA(cudaEventCreate(&t1));
-    MM_CUDA(cudaEventRecord(t0, e->stream));
+    // events, graph and exec are released on every exit path; a throw while
+    // capturing ends the capture so the engine stream stays usable
+    struct Res {
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        ~Res() {
+            if (ge) cudaGraphExecDestroy(ge);
+            if (g) cudaGraphDestroy(g);
+            if (t0) cudaEventDestroy(t0);
+            if (t1) cudaEventDestroy(t1);
+        }
+    } res;
+    MM_CUDA(cudaEventCreate(&res.t0));
+    MM_CUDA(cudaEventCreate(&res.t1));
+    MM_CUDA(cudaEventRecord(res.t0, e->stream));
+    // per-step finiteness check (ref: driver.cpp:68-71,108): receiver 0 when
+    // recording; without recording the same check on receiver 0 (or the source)
+    const bool rec_on = record && e->nrec > 0;
+    long long check = -1;
+    if (!rec_on) {
+        if (e->nrec > 0)
+            check = e->lay.off(e->rec_ijk[0], e->rec_ijk[1], e->rec_ijk[2]);
+        else if (src)
+            check = e->src_off(src);
+    }
     auto one_step = [&] {
         const RecParams rp{nullptr, e->rec_offs.ptr,
-                           e->traces.ptr + (size_t)first_sample * e->nrec, e->nrec, 0, bad};
-        e->full_step(0.0f, src, e->amps.ptr, step_dev, record && e->nrec > 0 ? &rp : nullptr);
+                           e->traces.ptr + (size_t)first_sample * e->nrec, rec_on ? e->nrec : 0, 0,
+                           bad};
+        e->full_step(0.0f, src, e->amps.ptr, step_dev, &rp, check);
     };
     // The first step runs eagerly (it also builds the lazily created work
     // lists); then the buffer rotation's period of three steps is captured
@@ -868,29 +1002,28 @@ int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src, in
     // the faster one on the device -- see step_graphs_enabled)
     const bool use_graph = nsteps - s >= 6 && e->step_graphs_enabled();
     if (use_graph) {
-        cudaGraph_t g = nullptr;
-        cudaGraphExec_t ge = nullptr;
         const long long l0 = g_launches.load();
         MM_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-        for (int k = 0; k < 3; ++k) one_step();  // rotation period: host state returns
-        MM_CUDA(cudaStreamEndCapture(e->stream, &g));
+        try {
+            for (int k = 0; k < 3; ++k) one_step();  // rotation period: host state returns
+        } catch (...) {
+            cudaStreamEndCapture(e->stream, &res.g);
+            throw;
+        }
+        MM_CUDA(cudaStreamEndCapture(e->stream, &res.g));
         const long long per_graph = g_launches.load() - l0;  // kernels in the graph
-        MM_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        MM_CUDA(cudaGraphInstantiate(&res.ge, res.g, 0));
         const int reps = (nsteps - s) / 3;
-        for (int k = 0; k < reps; ++k) MM_CUDA(cudaGraphLaunch(ge, e->stream));
+        for (int k = 0; k < reps; ++k) MM_CUDA(cudaGraphLaunch(res.ge, e->stream));
         e->steps += 3LL * reps - 3;  // capture advanced the host counter by 3
         s += 3 * reps;
-        MM_CUDA(cudaGraphExecDestroy(ge));
-        MM_CUDA(cudaGraphDestroy(g));
         note_launches(per_graph * (reps - 1));  // kernels executed by the replays
     }
     for (; s < nsteps; ++s) one_step();
-    MM_CUDA(cudaEventRecord(t1, e->stream));
-    MM_CUDA(cudaEventSynchronize(t1));
+    MM_CUDA(cudaEventRecord(res.t1, e->stream));
+    MM_CUDA(cudaEventSynchronize(res.t1));
     float ms = 0;
-    MM_CUDA(cudaEventElapsedTime(&ms, t0, t1));
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
+    MM_CUDA(cudaEventElapsedTime(&ms, res.t0, res.t1));
     if (device_ms) *device_ms = ms;
     int bad_h = INT_MAX;
     MM_CUDA(cudaMemcpy(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost));
@@ -899,6 +1032,51 @@ int mm_cd_run(mm_cd_engine* e, const float* amps, int nsteps, const int* src, in
                     "non-finite wavefield sample detected at time step " +
                         std::to_string(first_sample + bad_h),
                     first_sample + bad_h);
+    MM_API_END
+}
+
+int mm_cd_cpml_path(mm_cd_engine* e, char* buf, int cap) {
+    MM_API_BEGIN
+    use(e);
+    need(buf, "buf");
+    if (cap < 1) raise(ST_INVAL, "cap must be >= 1");
+    const char* v = (e->mode == MM_MODE_STRICT || !e->fast) ? "strict" : e->fast->cpml_path(e->params());
+    std::strncpy(buf, v, cap - 1);
+    buf[cap - 1] = 0;
+    MM_API_END
+}
+
+int mm_cd_kernel_timing(mm_cd_engine* e, int on) {
+    MM_API_BEGIN
+    use(e);
+    if (!e->fast) raise(ST_INVAL, "kernel timing needs a fast-mode engine");
+    MM_CUDA(cudaStreamSynchronize(e->stream));
+    e->fast->timer.reset();
+    e->fast->timer.on = on != 0;
+    MM_API_END
+}
+
+int mm_cd_kernel_times(mm_cd_engine* e, int cap, char (*names)[32], double* total_ms,
+                       long long* launches, int* n) {
+    MM_API_BEGIN
+    use(e);
+    need(n, "n");
+    *n = 0;
+    if (!e->fast) return MM_OK;
+    e->fast->timer.collect();
+    int i = 0;
+    for (const auto& kv : e->fast->timer.acc) {
+        if (i < cap) {
+            if (names) {
+                std::strncpy(names[i], kv.first.c_str(), 31);
+                names[i][31] = 0;
+            }
+            if (total_ms) total_ms[i] = kv.second.first;
+            if (launches) launches[i] = kv.second.second;
+        }
+        ++i;
+    }
+    *n = i;
     MM_API_END
 }
 

@@ -1,12 +1,17 @@
 // kernels_fast.cu -- MM_MODE_FAST step: plan (tensor maps, work lists) + launches.
 //
-// One step = k_p1 (CPML pass 1: psi, and dpsi_z of the z runs) -> k_bnd (pass 2
-// over the X and Y slabs) -> k_inner (the inner x-y box over every z: plain
-// update inside, pass 2 along z in the Z slabs) -> source injection, each
-// kernel persistent over the whole GPU, pulling (tile, z-chunk) work items.
-// Kernels: fast_pass1.cuh (k_p1), fast_boundary.cuh (k_bnd), fast_inner.cuh (k_inner).
-// When the fast CPML kernels cannot serve a layout (radius 8, or z runs closer
-// than 2R), pass 1 and the slabs run the strict kernels and k_inner the inner box.
+// One step = k_cpml (both CPML passes over the six damping slabs, one launch,
+// fast_cpml.cuh) on the step's stream || k_inner (the inner box, update_plain,
+// fast_inner.cuh) on a side stream -> the epilogue (engine.cu).  Each kernel
+// is persistent over the whole GPU and pulls (tile, z-chunk) work items.
+// Layouts k_cpml cannot serve (radius > 4, damping layers wider than its
+// 32-point tiles, grids whose layers lie within a tile of each other) run the
+// two-pass path: k_p1 (pass 1: psi, and dpsi_z of the z runs, fast_pass1.cuh)
+// -> k_bnd (pass 2 over the X and Y slabs, fast_boundary.cuh) with k_inner
+// (and the Z slabs); and where those cannot either (z runs closer than 2R),
+// the strict kernels.  The sub-phase API (pass1 / update / update_ranges)
+// always runs the two-pass kernels, which keep the reference's pass
+// boundaries (psi is updated by pass 1, not by the boundary update).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -19,6 +24,7 @@
 #include <vector>
 
 #include "fast_boundary.cuh"
+#include "fast_cpml.cuh"
 #include "fast_inner.cuh"
 #include "fast_pass1.cuh"
 #include "mm_fast.hpp"
@@ -55,16 +61,13 @@ CUtensorMap make_map(const void* base, long long dx, long long dy, long long dz,
     const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     // L2 promotion: 128B by default (boxes start 16B- but not always
-    // 256B-aligned; 256B promotion would fetch unused bytes).  MM_L2PROMO=0..3
-    // selects none/64B/128B/256B for experiments.
-    static const CUtensorMapL2promotion promo = [] {
-        const char* e = std::getenv("MM_L2PROMO");
-        const int v = e ? std::atoi(e) : 2;
-        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-               : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-               : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                        : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    }();
+    // 256B-aligned; 256B promotion would fetch unused bytes).  Tuning
+    // "l2_promo" 0..3 selects none/64B/128B/256B for experiments.
+    const long long v = tuning("l2_promo");
+    const CUtensorMapL2promotion promo = v == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                         : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                         : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                  : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base),
                                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                    CU_TENSOR_MAP_SWIZZLE_NONE, promo,
@@ -187,10 +190,13 @@ class FastPlanR final : public FastPlan {
     static constexpr bool kBnd = BC::SMEM <= 227 * 1024;  // TMA boundary kernel fits
     static constexpr bool kZs = ZSlabCfg<R>::SMEM <= 227 * 1024;  // optional Z-slab kernel
     static constexpr bool kP1 = P1C::SMEM <= 200 * 1024;
+    static constexpr int RC = R <= 4 ? R : 4;  // (k_cpml is instantiated for R <= 4 only)
+    using CC = CpmlCfg<RC>;
+    static constexpr bool kCpml = R <= 4 && CC::SMEM <= 227 * 1024;
 
 public:
-    FastPlanR(const Layout& lay, int device, float* const bufs[3], const float* cv)
-        : lay_(lay), device_(device) {
+    FastPlanR(const Layout& lay, int device, float* const bufs[3], const float* cv, int order)
+        : lay_(lay), device_(device), order_(order) {
         for (int b = 0; b < 3; ++b) {
             bufs_[b] = bufs[b];
             in_halo_[b] = field_map(lay, bufs[b], IC::BX, IC::BY);
@@ -200,32 +206,39 @@ public:
             p1x_[b] = field_map(lay, bufs[b], P1C::BXX, P1C::TY);
             p1y_[b] = field_map(lay, bufs[b], P1C::TX, P1C::BYY);
             p1z_[b] = field_map(lay, bufs[b], P1C::TX, P1C::TY);
+            if constexpr (kCpml) {
+                cm_pc_[b] = field_map(lay, bufs[b], CC::BX, CC::BY);
+                cm_tile_[b] = field_map(lay, bufs[b], CC::TX, CC::TY);
+            }
         }
         cv_in_ = field_map(lay, cv, IC::TX, IC::TY);
         cv_bd_ = field_map(lay, cv, BC::TX, BC::TY);
-        const char* ord = std::getenv("MM_FAST_ORDER");
-        // MM_FAST_ORDER: 2 (default) bit-exact reference order, 1 FMA, 0 factored
-        order_ = ord ? std::max(0, std::min(2, std::atoi(ord))) : 2;
-        // z-chunk targets (planes per work item) of the two persistent kernels
-        auto envf = [](const char* k, double d) {
-            const char* v = std::getenv(k);
-            return v ? std::max(1.0, std::atof(v)) : d;
-        };
-        inner_zt_ = envf("MM_INNER_ZT", 48.0);
-        bnd_zt_ = envf("MM_BND_ZT", 12.0);
-        p1_zt_ = envf("MM_P1_ZT", 16.0);
+        if constexpr (kCpml) cm_cv_ = field_map(lay, cv, CC::TX, CC::TY);
+        // z-chunk targets (planes per work item) of the persistent kernels
+        inner_zt_ = (double)std::max(1LL, tuning("inner_zt"));
+        bnd_zt_ = (double)std::max(1LL, tuning("bnd_zt"));
+        p1_zt_ = (double)std::max(1LL, tuning("p1_zt"));
+        cpml_zt_ = (int)tuning("cpml_zt");
+        cpml_on_ = kCpml && tuning("cpml_fused") != 0;
         // Z slabs: 0 = k_bnd tiles, 1 = k_zslab over the Z slabs after k_inner,
         // 2 = k_zslab over whole z columns of the inner box (instead of k_inner)
-        if (const char* zm = std::getenv("MM_ZSLABS")) zmode_ = std::max(0, std::min(2, std::atoi(zm)));
+        const long long zm = tuning("zslabs");
+        if (zm >= 0) zmode_ = (int)std::min(2LL, zm);
         if (!kZs) zmode_ = 0;
-        { const char* ov = std::getenv("MM_OVERLAP"); overlap_ = !ov || ov[0] != '0'; }
+        if (zmode_ != 0) cpml_on_ = false;  // (k_cpml does the Z slabs itself)
+        overlap_ = tuning("overlap") != 0;
+        inner_late_ = (int)tuning("inner_late");
+        dbg_ = tuning("debug_sync") == 1;
+        bnd_kinds_ = (int)tuning("bnd_kinds");
+        bnd_cap_ = tuning("bnd_ctas") > 0 ? (int)tuning("bnd_ctas") : 1 << 30;
+        p1_axes_ = (int)tuning("p1_axes");
         // side streams at the lowest priority: pass 1's z runs (on the step's
         // stream, the critical path) are scheduled first
         int prio_lo = 0, prio_hi = 0;
         MM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         MM_CUDA(cudaStreamCreateWithPriority(&p1_side_, cudaStreamNonBlocking,
-                                             main_stream_priority() >= 2 ? prio_hi : prio_lo));
-        { const char* e = std::getenv("MM_PDL"); pdl_ = !e || e[0] != '0'; }
+                                             tuning("main_prio") >= 2 ? prio_hi : prio_lo));
+        pdl_ = tuning("pdl") != 0;
         MM_CUDA(cudaEventCreateWithFlags(&p1_fork_, cudaEventDisableTiming));
         MM_CUDA(cudaEventCreateWithFlags(&p1_join_, cudaEventDisableTiming));
         if (overlap_) {
@@ -239,15 +252,24 @@ public:
         // instruction cache; the column kernel (smem z window) serves the inner
         // box and the Z slabs instead
         col_inner_ = kZs && R > 4;
-        if (col_inner_ && !std::getenv("MM_ZSLABS")) zmode_ = 2;
+        if (col_inner_ && zm < 0) zmode_ = 2;
         cudaDeviceProp prop;
         MM_CUDA(cudaGetDeviceProperties(&prop, device));
         sms_ = prop.multiProcessorCount;
-        for (auto fn : {k_inner<R, 0>, k_inner<R, 1>, k_inner<R, 2>})
+        for (auto fn : {k_inner<R, 1>, k_inner<R, 2>})
             MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)IC::SMEM));
+        if constexpr (kCpml) {
+            for (auto fn : {k_cpml<RC, 1>, k_cpml<RC, 2>})
+                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)CC::SMEM));
+            int per = 0;
+            MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cpml<RC, 2>, CC::NT,
+                                                                  CC::SMEM));
+            cpml_per_sm_ = std::max(1, per);
+        }
         if constexpr (kZs)
-            for (auto fn : {k_zslab<R, 0>, k_zslab<R, 1>, k_zslab<R, 2>})
+            for (auto fn : {k_zslab<R, 1>, k_zslab<R, 2>})
                 MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)ZSlabCfg<R>::SMEM));
         int per_sm = 0;
@@ -321,49 +343,84 @@ public:
 
     void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
               const int* step_dev, cudaStream_t s) override {
+        if (use_cpml(p)) {
+            // k_cpml (both CPML passes, all slabs) on the step's stream; the
+            // interior kernel, which needs no CPML state, beside it on the side
+            // stream (a second branch of a captured graph), joined before the
+            // epilogue
+            if (overlap_) {
+                MM_CUDA(cudaEventRecord(fork_, s));
+                MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+                const int ti = timer.begin("inner", side_);
+                launch_inner(p, 0, lay_.n[2], kInnerOnly, side_);
+                timer.end(ti, side_);
+                MM_CUDA(cudaEventRecord(join_, side_));
+            }
+            dbg(s, "inner(side)", overlap_ ? side_ : nullptr);
+            const int tc = timer.begin("cpml", s);
+            launch_cpml(p, ZRanges{{0, lay_.n[2]}}, s);
+            timer.end(tc, s);
+            dbg(s, "cpml", nullptr);
+            if (overlap_) {
+                MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
+            } else {
+                const int ti = timer.begin("inner", s);
+                launch_inner(p, 0, lay_.n[2], kInnerOnly, s);
+                timer.end(ti, s);
+            }
+            if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
+            return;
+        }
         const bool fc = fast_cpml(p);
         const int imode = fc && zmode_ != 0 ? kFull : kInnerOnly;
         // (the Z-slab planes read dpsi_z from pass 1: no overlap then)
         const bool ov = overlap_ && imode == kInnerOnly;
-        static const int inner_late = [] {
-            const char* e = std::getenv("MM_INNER_LATE");
-            return e ? std::atoi(e) : 0;
-        }();
         auto fork_inner = [&] {
             // the interior kernel needs no CPML state: it runs on a second
             // stream beside pass 1 -> boundary and takes SMs as their tails free
             // them (a second branch of the captured graph)
             MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+            const int ti = timer.begin("inner", side_);
             launch_inner(p, 0, lay_.n[2], imode, side_);
+            timer.end(ti, side_);
             MM_CUDA(cudaEventRecord(join_, side_));
         };
         if (ov) MM_CUDA(cudaEventRecord(fork_, s));  // the step's start
-        if (ov && inner_late == 0) fork_inner();
+        if (ov && inner_late_ == 0) fork_inner();
         dbg(s, "inner(side)", ov ? side_ : nullptr);
+        const int t1 = timer.begin("pass1", s);
         launch_pass1(p, 0, lay_.n[2], s);
+        timer.end(t1, s);
         dbg(s, "pass1", p1_side_);
-        if (ov && inner_late == 1) fork_inner();  // (issue order only: still from the start)
+        if (ov && inner_late_ == 1) fork_inner();  // (issue order only: still from the start)
+        const int t2 = timer.begin("boundary", s);
         if (fc)
             launch_boundary(p, 0, lay_.n[2], s);
         else
             strict_update(p, 2, 0, lay_.n[2], s);
+        timer.end(t2, s);
         dbg(s, "boundary", nullptr);
-        if (ov && inner_late == 2) fork_inner();
-        if (ov)
+        if (ov && inner_late_ == 2) fork_inner();
+        if (ov) {
             MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
-        else
+        } else {
+            const int ti = timer.begin("inner", s);
             launch_inner(p, 0, lay_.n[2], imode, s);
+            timer.end(ti, s);
+        }
         dbg(s, "inner", nullptr);
         if (src_off >= 0) launch_inject(p.pn, p.cv, src_off, amp, amp_dev, step_dev, s);
     }
-    // MM_DEBUG_SYNC=kernels: synchronize after each kernel of the step and name
-    // the one that faulted (diagnostics only)
+
+    const char* cpml_path(const StepParams& p) override {
+        if (use_cpml(p)) return "cpml";
+        return fast_cpml(p) ? "two-pass" : "strict";
+    }
+
+    // tuning "debug_sync" == 1: synchronize after each kernel of the step and
+    // name the one that faulted (diagnostics only)
     void dbg(cudaStream_t s, const char* what, cudaStream_t s2) {
-        static const bool on = [] {
-            const char* e = std::getenv("MM_DEBUG_SYNC");
-            return e && std::strcmp(e, "kernels") == 0;
-        }();
-        if (!on) return;
+        if (!dbg_) return;
         cudaError_t e = s2 ? cudaStreamSynchronize(s2) : cudaSuccess;
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess)
@@ -484,11 +541,7 @@ private:
         regions(p, inner, slabs);
         std::vector<Item> items;  // one per tile
         w.nbox = 0;
-        // MM_BND_KINDS (profiling only): bit mask of the slab kinds to update
-        static const int kinds = [] {
-            const char* e = std::getenv("MM_BND_KINDS");
-            return e ? std::atoi(e) : 7;
-        }();
+        const int kinds = bnd_kinds_;  // (profiling: slab kinds to update)
         for (const auto& s : slabs) {
             if ((s.first / 2 == 2 && zmode_ != 0) || !((kinds >> (s.first / 2)) & 1)) continue;
             const Box& b = s.second;
@@ -571,17 +624,13 @@ private:
                 constexpr size_t zsm = ZSlabCfg<R>::SMEM;
                 if (order_ == 2)
                     k_zslab<R, 2><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
-                else if (order_ == 1)
-                    k_zslab<R, 1><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
                 else
-                    k_zslab<R, 0><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+                    k_zslab<R, 1><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
             }
         } else if (order_ == 2) {
             k_inner<R, 2><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
-        } else if (order_ == 1) {
-            k_inner<R, 1><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
         } else {
-            k_inner<R, 0><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
+            k_inner<R, 1><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
         }
         note_launches(1);
         MM_CUDA(cudaGetLastError());
@@ -627,7 +676,14 @@ private:
                 if (a == 1) maps_.psi[1][sd] = run_map(lay_, r, a, r.psi, BC::TX, BC::BY);  // y halo
                 maps_.zeta[a][sd] = run_map(lay_, r, a, r.zeta, BC::TX, BC::TY);
                 p1maps_.psi[a][sd] = run_map(lay_, r, a, r.psi, P1C::TX, P1C::TY);
+                if constexpr (kCpml) {
+                    cmaps_.psi[a][sd] = run_map(lay_, r, a, r.psi, CC::TX, CC::TY);
+                    cmaps_.zeta[a][sd] = run_map(lay_, r, a, r.zeta, CC::TX, CC::TY);
+                }
             }
+        // the fused kernel's tiles follow the runs' extents
+        cgeo_.built = false;
+        cpml_cache_.clear();
         runs_valid_ = true;
     }
 
@@ -676,12 +732,8 @@ private:
             bp_.pn = p.pn;
             bp_.segs = w.segs.ptr;
             bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
-            // MM_BND_CTAS (diagnostics): cap the CTA count (more items per CTA)
-            static const int cap = [] {
-                const char* e = std::getenv("MM_BND_CTAS");
-                return e ? std::max(1, std::atoi(e)) : 1 << 30;
-            }();
-            const int ctas = std::min(w.ctas, cap);
+            // tuning "bnd_ctas" (diagnostics): cap the CTA count (more items per CTA)
+            const int ctas = std::min(w.ctas, bnd_cap_);
             if (order_ == 2)
                 launch_pdl(k_bnd<R, 2>, ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
             else
@@ -706,11 +758,7 @@ private:
                 Pass1Work& e = pass1_cache_[key];
                 std::vector<Item> tiles;
                 std::vector<int4> zitems;
-                // MM_P1_AXES (profiling only): bit mask of the run axes to update
-                static const int axes = [] {
-                    const char* e = std::getenv("MM_P1_AXES");
-                    return e ? std::atoi(e) : 7;
-                }();
+                const int axes = p1_axes_;  // (profiling: run axes to update)
                 for (int ax = 0; ax < 3; ++ax)
                     for (int side = 0; side < 2; ++side) {
                         const CpmlRun& r = p.run[ax][side];
@@ -808,6 +856,210 @@ private:
         }
     }
 
+    // ---------------------------------------------------------------- k_cpml
+    // 1-D tile partition of [0, n) along x (margin 0; the tile of a run starts
+    // at its 16-byte-aligned origin) or y (margin R) for the fused kernel:
+    // each part = physical tile start t0, owned range [lo, hi), damping run
+    // side (-1: none).  Rules (fast_cpml.cuh): a run lies inside its tile, the
+    // rows within `margin` of it are owned by that tile only, and no other
+    // tile of the partition holds a run.  false: the two-pass path serves it.
+    struct Part {
+        int t0, lo, hi, side;
+    };
+    static bool cpml_parts(int n, const CpmlRun& L, const CpmlRun& H, int margin, bool xaxis,
+                           std::vector<Part>& out) {
+        constexpr int T = CC::TX;  // == CC::TY
+        out.clear();
+        const bool hl = L.hi > L.lo, hh = H.hi > H.lo;
+        if (hl && (L.lo != 0 || L.org != 0)) return false;
+        const int c1 = hl ? std::min(T, n) : 0;
+        int t0h = n, own_h = n;
+        if (hh) {
+            t0h = xaxis ? H.org : std::max(n - T, 0);
+            own_h = xaxis ? H.org : std::max(t0h, c1);
+            if (H.hi > t0h + T) return false;         // the run fits in its tile
+            if (own_h > H.lo - margin) return false;  // run + margin owned by its tile
+        }
+        const int c1e = std::min(c1, own_h);
+        if (hl && L.hi + margin > c1e) return false;
+        if (hl) out.push_back(Part{0, 0, c1e, 0});
+        for (int m = c1e; m < own_h; m += T) out.push_back(Part{m, m, std::min(m + T, own_h), -1});
+        if (hh) out.push_back(Part{t0h, own_h, n, 1});
+        return true;
+    }
+
+    // Tiles of the fused kernel (built once per CPML run geometry).
+    struct CpmlGeo {
+        bool built = false, ok = false;
+        std::vector<CTile> tiles;
+        std::vector<char> full;  // 1: every plane; 0: the Z-slab planes only
+        DArr<CTile> dtiles;
+        std::vector<std::pair<int, int>> forb;  // forbidden chunk boundaries (a, b), open
+        Box inner{};
+    };
+    CpmlGeo& cpml_geo(const StepParams& p) {
+        CpmlGeo& g = cgeo_;
+        if (g.built) return g;
+        g.built = true;
+        g.ok = false;
+        if constexpr (kCpml) {
+            // x and y are whole in every engine the fused kernel serves (the
+            // multi-GPU path cuts z only)
+            if (p.goff[0] != 0 || p.goff[1] != 0 || lay_.n[0] != p.gn[0] || lay_.n[1] != p.gn[1])
+                return g;
+            std::vector<Part> xp, yp;
+            if (!cpml_parts(lay_.n[0], p.run[0][0], p.run[0][1], 0, true, xp)) return g;
+            if (!cpml_parts(lay_.n[1], p.run[1][0], p.run[1][1], R, false, yp)) return g;
+            const CpmlRun &z0 = p.run[2][0], &z1 = p.run[2][1];
+            const bool h0 = z0.hi > z0.lo, h1 = z1.hi > z1.lo;
+            // a Z slab sees its own z run only: the other run must lie R away
+            if (h0 && h1 && z1.lo - z0.hi < R) return g;
+            std::vector<std::pair<int, Box>> slabs;
+            regions(p, g.inner, slabs);
+            const Box& I = g.inner;
+            g.forb.clear();
+            for (const CpmlRun* r : {&z0, &z1})
+                if (r->hi > r->lo) g.forb.emplace_back(r->lo - R, r->hi + R);
+            g.tiles.clear();
+            g.full.clear();
+            for (const Part& a : xp)
+                for (const Part& b : yp) {
+                    if (a.hi <= a.lo || b.hi <= b.lo) continue;
+                    const bool xyslab = a.lo < I.lo[0] || a.hi > I.hi[0] || b.lo < I.lo[1] ||
+                                        b.hi > I.hi[1] || I.hi[0] <= I.lo[0] || I.hi[1] <= I.lo[1];
+                    const bool zslab = I.lo[2] > 0 || I.hi[2] < lay_.n[2];
+                    if (!xyslab && !zslab) continue;
+                    g.tiles.push_back(CTile{a.t0, a.hi, b.t0, b.hi, a.side, b.side, a.lo, b.lo});
+                    g.full.push_back(xyslab ? 1 : 0);
+                }
+            g.dtiles.set(g.tiles, stream_setup_);
+            g.ok = true;
+        }
+        return g;
+    }
+
+    bool use_cpml(const StepParams& p) {
+        if (!cpml_on_) return false;
+        refresh_run_maps(p);  // (rebuilds the tiles when the runs changed)
+        return cpml_geo(p).ok;
+    }
+
+    // [a, b) cut into chunks of about `target` planes, no boundary inside a
+    // forbidden zone (within R of a z run: chunks update psi_z in place)
+    static void chunk_planes(int a, int b, int target, const std::vector<std::pair<int, int>>& forb,
+                             std::vector<std::pair<int, int>>& out) {
+        int zb = a;
+        while (zb < b) {
+            int ze = std::min(b, zb + std::max(1, target));
+            for (bool moved = true; moved;) {
+                moved = false;
+                for (const auto& f : forb)
+                    if (ze > f.first && ze < f.second && ze < b) {
+                        ze = std::min(b, f.second);
+                        moved = true;
+                    }
+            }
+            out.emplace_back(zb, ze);
+            zb = ze;
+        }
+    }
+
+    struct CpmlWork {
+        DArr<int4> items;
+        DArr<int> ctr;
+        int nitems = 0, ctas = 0;
+    };
+    CpmlWork& cpml_work(const StepParams& p, const ZRanges& ranges) {
+        const auto key = wkey(ranges, 0);
+        auto it = cpml_cache_.find(key);
+        if (it != cpml_cache_.end()) return it->second;
+        CpmlWork& w = cpml_cache_[key];
+        CpmlGeo& g = cpml_geo(p);
+        const int nz = lay_.n[2];
+        // the planes of every tile within this launch's ranges
+        std::vector<std::pair<int, std::pair<int, int>>> segs;  // (tile, [a, b))
+        long long planes = 0;
+        for (size_t t = 0; t < g.tiles.size(); ++t) {
+            std::vector<std::pair<int, int>> zs;
+            if (g.full[t])
+                zs.emplace_back(0, nz);
+            else {
+                zs.emplace_back(0, g.inner.lo[2]);
+                zs.emplace_back(g.inner.hi[2], nz);
+            }
+            for (const auto& z : zs)
+                for (const auto& rg : ranges) {
+                    const int a = std::max(z.first, rg.first), b = std::min(z.second, rg.second);
+                    if (b > a) {
+                        segs.push_back({(int)t, {a, b}});
+                        planes += b - a;
+                    }
+                }
+        }
+        const int slots = sms_ * cpml_per_sm_;
+        // about two items per CTA, at least 12 planes each (items pay a 2R- or
+        // 4R-plane warm-up of the z window)
+        int target = cpml_zt_ > 0 ? cpml_zt_
+                                  : (int)std::max<long long>(12, (planes + 2LL * slots - 1) / (2LL * slots));
+        std::vector<std::pair<int, int4>> items;  // (z_begin, item)
+        for (const auto& sg : segs) {
+            std::vector<std::pair<int, int>> ch;
+            chunk_planes(sg.second.first, sg.second.second, target, g.forb, ch);
+            for (const auto& c : ch) items.push_back({c.first, make_int4(sg.first, c.first, c.second, 0)});
+        }
+        // chunk-major: the items in flight are neighbouring tiles at nearby
+        // depths (their p_cur halo planes meet in L2)
+        std::stable_sort(items.begin(), items.end(),
+                         [](const auto& a, const auto& b) { return a.first < b.first; });
+        std::vector<int4> v;
+        for (const auto& i : items) v.push_back(i.second);
+        w.nitems = (int)v.size();
+        w.ctas = std::max(1, std::min(slots, w.nitems));
+        w.items.set(v, stream_setup_);
+        w.ctr.set(std::vector<int>{0, 0}, stream_setup_);
+        return w;
+    }
+
+    void launch_cpml(const StepParams& p, const ZRanges& zr, cudaStream_t s) {
+        if constexpr (kCpml) {
+            refresh_run_maps(p);
+            CpmlGeo& g = cpml_geo(p);
+            if (!g.ok) raise(ST_INVAL, "k_cpml cannot serve this layout");
+            CpmlWork& w = cpml_work(p, zr);
+            if (w.nitems == 0) return;
+            CpmlMaps M = cmaps_;
+            M.pc = cm_pc_[buf_index(p.pc)];
+            M.pp = cm_tile_[buf_index(p.pp)];
+            M.cv = cm_cv_;
+            CpmlParams P;
+            std::memset(&P, 0, sizeof P);
+            P.lay = lay_;
+            for (int a = 0; a < 3; ++a) {
+                P.ilo[a] = g.inner.lo[a];
+                P.ihi[a] = g.inner.hi[a];
+                P.run[a][0] = p.run[a][0];
+                P.run[a][1] = p.run[a][1];
+                P.ta[a] = p.ta[a];
+                P.tb[a] = p.tb[a];
+                P.tik[a] = p.tik[a];
+                for (int m = 0; m < kMaxR; ++m) {
+                    P.c2[a][m] = p.c2[a][m];
+                    P.c1[a][m] = p.c1[a][m];
+                }
+            }
+            P.tiles = g.dtiles.ptr;
+            P.items = w.items.ptr;
+            P.wq = WorkQueue{w.ctr.ptr, w.nitems};
+            P.pn = p.pn;
+            if (order_ == 2)
+                k_cpml<RC, 2><<<w.ctas, CC::NT, CC::SMEM, s>>>(M, P);
+            else
+                k_cpml<RC, 1><<<w.ctas, CC::NT, CC::SMEM, s>>>(M, P);
+            note_launches(1);
+            MM_CUDA(cudaGetLastError());
+        }
+    }
+
     struct Pass1Work {
         RunDesc rd[6];
         int nrd = 0;
@@ -819,8 +1071,14 @@ private:
 
     Layout lay_;
     int device_;
-    int sms_ = 148, inner_per_sm_ = 1, bnd_per_sm_ = 1;
     int order_ = 2;
+    int sms_ = 148, inner_per_sm_ = 1, bnd_per_sm_ = 1, cpml_per_sm_ = 1;
+    bool cpml_on_ = false, dbg_ = false;
+    int cpml_zt_ = 0, inner_late_ = 0, bnd_kinds_ = 7, bnd_cap_ = 1 << 30, p1_axes_ = 7;
+    CUtensorMap cm_pc_[3], cm_tile_[3], cm_cv_;
+    CpmlMaps cmaps_{};
+    CpmlGeo cgeo_;
+    std::map<std::vector<int>, CpmlWork> cpml_cache_;
     double inner_zt_ = 48.0, bnd_zt_ = 48.0;
     int zmode_ = 0;
     bool pdl_ = true;
@@ -850,11 +1108,11 @@ private:
 }  // namespace
 
 std::unique_ptr<FastPlan> make_fast_plan(const Layout& lay, int device, float* const bufs[3],
-                                         const float* cv) {
+                                         const float* cv, int order) {
     switch (lay.r) {
-        case 2: return std::make_unique<FastPlanR<2>>(lay, device, bufs, cv);
-        case 4: return std::make_unique<FastPlanR<4>>(lay, device, bufs, cv);
-        case 8: return std::make_unique<FastPlanR<8>>(lay, device, bufs, cv);
+        case 2: return std::make_unique<FastPlanR<2>>(lay, device, bufs, cv, order);
+        case 4: return std::make_unique<FastPlanR<4>>(lay, device, bufs, cv, order);
+        case 8: return std::make_unique<FastPlanR<8>>(lay, device, bufs, cv, order);
         default: return nullptr;  // other radii run the strict kernels
     }
 }

@@ -25,11 +25,16 @@ public:
     // One whole step (pass 1, update, source injection); src_off < 0: no source.
     virtual void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
                       const int* step_dev, cudaStream_t s) = 0;
+    // The kernel the step uses for the damping slabs: "cpml" (fused one-pass
+    // k_cpml), "two-pass" (k_p1 + k_bnd) or "strict".
+    virtual const char* cpml_path(const StepParams& p) = 0;
+    KernelTimer timer;  // per-kernel events around the step's launches (off by default)
 };
 
 // nullptr when the fast kernels cannot serve this layout (the engine then
 // runs the strict kernels, which are exact for every radius).
+// order: 2 = reference order, every operation rounded (bit-exact); 1 = FMA.
 std::unique_ptr<FastPlan> make_fast_plan(const Layout& lay, int device, float* const bufs[3],
-                                         const float* cv);
+                                         const float* cv, int order);
 
 }  // namespace mmb

@@ -12,6 +12,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -37,8 +38,13 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 
 // Counts kernel launches issued through the library (evidence for bench.py).
 void note_launches(long long n);
-int main_stream_priority();  // MM_MAIN_PRIO (engine.cu)
 long long launches_so_far();
+
+// Process-wide tuning parameters (mm_set_tuning in the C ABI; engine.cu).
+// The library never reads the environment: every parameter has a product
+// default, and tests / experiments change one explicitly before creating an
+// engine (most are read when an engine or its fast plan is created).
+long long tuning(const char* name);
 
 // C-ABI error plumbing (engine.cu): records the thread-local message/step
 // behind mm_last_error() and returns the status code.
@@ -153,6 +159,29 @@ struct TraceCopier {
     }
 };
 
+// Per-kernel CUDA-event timing of the launches of a step (bench evidence:
+// the dominant kernel's duration inside the real, concurrent step).  Off by
+// default; begin/end record events on the launching stream.
+struct KernelTimer {
+    bool on = false;
+    int begin(const char* name, cudaStream_t s);  // -1 when off
+    void end(int idx, cudaStream_t s);
+    // waits for the recorded events and adds their durations to `acc`
+    void collect();
+    void reset();
+    std::map<std::string, std::pair<double, long long>> acc;  // name -> (total ms, launches)
+    ~KernelTimer();
+
+private:
+    struct Rec {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending_;
+    std::vector<cudaEvent_t> pool_;
+    cudaEvent_t get();
+};
+
 struct Layout {
     int n[3];
     int r, L, P, ey, ez;
@@ -231,6 +260,7 @@ struct Epilogue {
     bool fs;               // free surface at local z = 0
     Layout lay;
     RecParams rec;         // nrec = 0: no sampling (rec.p is ignored: p)
+    long long check_off;   // >= 0 and rec.nrec == 0: finiteness check of this point into rec.bad_step
     int* done;             // block ticket (zero between launches)
 };
 

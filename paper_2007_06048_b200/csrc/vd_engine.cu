@@ -247,7 +247,7 @@ struct FastVd {
         const int slots = sms * std::max(ov, op);
         int nch = std::max((L.n[2] + 19) / 20, (6 * slots + tx * ty - 1) / (tx * ty));
         nch = std::max(1, std::min(nch, std::max(1, L.n[2] / 8)));
-        if (const char* e = std::getenv("MM_VD_ZCHUNKS")) nch = std::max(1, std::atoi(e));
+        if (tuning("vd_zchunks") > 0) nch = (int)tuning("vd_zchunks");
         std::vector<int4> it;
         for (int c = 0; c < nch; ++c) {
             const int zb = (int)((long long)L.n[2] * c / nch), ze = (int)((long long)L.n[2] * (c + 1) / nch);
@@ -260,10 +260,10 @@ struct FastVd {
         ctr.alloc_zero(4, s);
         grid_v = std::min(nitems, sms * ov);
         grid_p = std::min(nitems, sms * op);
-        // MM_VD_CTAS (diagnostics): cap the CTA count (long item sequences per CTA)
-        if (const char* e = std::getenv("MM_VD_CTAS")) {
-            grid_v = std::min(grid_v, std::max(1, std::atoi(e)));
-            grid_p = std::min(grid_p, std::max(1, std::atoi(e)));
+        // tuning "vd_ctas" (diagnostics): cap the CTA count (long item sequences per CTA)
+        if (const long long cap = tuning("vd_ctas"); cap > 0) {
+            grid_v = std::min(grid_v, (int)cap);
+            grid_p = std::min(grid_p, (int)cap);
         }
     }
 
@@ -621,8 +621,8 @@ int mm_vd_create(const mm_grid* grid, const float* vp, const float* rho,
     e->from_host(dtbh.data(), e->dtb.ptr);
     e->setup_cpml();
     e->counters.alloc_zero(3, e->stream);  // + the epilogue's block ticket
-    if (const char* zc = std::getenv("MM_VD_ZC")) e->zc = std::max(1, std::atoi(zc));
-    if (!std::getenv("MM_VD_SIMPLE")) {
+    if (tuning("vd_zc") > 0) e->zc = (int)tuning("vd_zc");
+    if (!tuning("vd_simple")) {
         float* const vv[3] = {e->v[0].ptr, e->v[1].ptr, e->v[2].ptr};
         e->fast = vd::make_fast_vd(e->lay, e->p.ptr, vv, e->ir.ptr, e->dtb.ptr, device, e->stream);
     }
@@ -833,7 +833,7 @@ int mm_vd_run(mm_vd_engine* e, const float* amps, int nsteps, const int* src, in
     // The fields update in place, so one step is captured as a CUDA graph and
     // replayed; per-step values come through the device step counter.
     int s = 0;
-    const bool use_graph = nsteps >= 4 && std::getenv("MM_NO_GRAPH") == nullptr;
+    const bool use_graph = nsteps >= 4 && tuning("step_graph") != 0;
     if (use_graph) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;

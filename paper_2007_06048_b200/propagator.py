@@ -21,7 +21,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import MM_MODE_FAST, MM_MODE_STRICT, check, lib
+from ._lib import MM_MODE_FAST, MM_MODE_FAST_FMA, MM_MODE_STRICT, check, lib
 from .numerics import AxisCpml, CpmlProfile, Grid3D, make_grid
 
 _i3 = C.c_int * 3
@@ -52,7 +52,7 @@ class EngineOptions:  # ref: propagator.hpp:23-30 (same defaults)
         return o
 
 
-_MODES = {"fast": MM_MODE_FAST, "strict": MM_MODE_STRICT}
+_MODES = {"fast": MM_MODE_FAST, "strict": MM_MODE_STRICT, "fast_fma": MM_MODE_FAST_FMA}
 
 
 class AcousticCdEngine:
@@ -235,6 +235,31 @@ class AcousticCdEngine:
                               _i3(*src) if src is not None else None, int(record),
                               int(first_sample), C.byref(ms)))
         return ms.value
+
+    def cpml_path(self) -> str:
+        """Kernels of a full step's damping-slab update: "cpml" (fused one-pass),
+        "two-pass" or "strict"."""
+        buf = C.create_string_buffer(32)
+        check(lib().mm_cd_cpml_path(self._h, buf, 32))
+        return buf.value.decode()
+
+    # -- per-kernel timing (bench evidence) ------------------------------
+    def kernel_timing(self, on: bool = True):
+        """Bracket every kernel of the following steps with CUDA events on its
+        own stream (steps issue eagerly while on); clears the totals."""
+        check(lib().mm_cd_kernel_timing(self._h, int(bool(on))))
+
+    def kernel_times(self) -> dict:
+        """{kernel name: (total ms, launches)} since kernel_timing(True)."""
+        n = C.c_int()
+        check(lib().mm_cd_kernel_times(self._h, 0, None, None, None, C.byref(n)))
+        k = n.value
+        names = (C.c_char * 32 * max(k, 1))()
+        ms = (C.c_double * max(k, 1))()
+        cnt = (C.c_longlong * max(k, 1))()
+        check(lib().mm_cd_kernel_times(self._h, k, C.cast(names, C.c_void_p), ms, cnt,
+                                       C.byref(n)))
+        return {names[i].value.decode(): (ms[i], cnt[i]) for i in range(k)}
 
     # -- multi-GPU plumbing ----------------------------------------------
     def stream_handle(self) -> int:

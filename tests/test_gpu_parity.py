@@ -1,14 +1,18 @@
 """GPU parity: the CUDA engine (through the C ABI) against the reference's own
 golden vectors and the pinned CPU oracle.
 
-Bar (BASELINE.json north_star): MM_MODE_STRICT is bit-identical to the CPU
-reference; MM_MODE_FAST (FMA-contracted, reassociated stencil) keeps the final
-wavefield within relative L2 <= 1e-5 of it (max-abs reported in the message).
+Bar: MM_MODE_STRICT and MM_MODE_FAST (the default: TMA kernels, reference
+association order, every operation separately rounded) are bit-identical to
+the CPU reference; MM_MODE_FAST_FMA (FMA-contracted) keeps the final
+wavefield within the north_star tolerance, relative L2 <= 1e-5 (max-abs
+reported in the message).
 """
 import os
 
 import numpy as np
 import pytest
+
+from paper_2007_06048_b200._lib import tuned
 
 from conftest import ROOT, load_golden
 
@@ -64,8 +68,8 @@ def test_strict_engine_bitwise_vs_reference_golden(mm, name):
 
 
 @pytest.mark.parametrize("name", ENGINE_CASES)
-def test_fast_engine_within_tolerance_vs_reference_golden(mm, name):
-    g, e, surf = run_golden(mm, name, "fast")
+def test_fast_fma_engine_within_tolerance_vs_reference_golden(mm, name):
+    g, e, surf = run_golden(mm, name, "fast_fma")
     p = e.pressure()
     err = rel_l2(p, g["p_cur"])
     maxabs = float(np.abs(p.astype(np.float64) - g["p_cur"]).max())
@@ -77,9 +81,6 @@ def test_fast_engine_within_tolerance_vs_reference_golden(mm, name):
 def test_fast_engine_bitwise_vs_reference_golden(mm, name):
     """The default fast kernels keep the reference's association order with
     every operation separately rounded: bit-identical, like the strict path."""
-    import os
-    if os.environ.get("MM_FAST_ORDER", "2") != "2":
-        pytest.skip("fast kernels built for a reassociated order")
     g, e, surf = run_golden(mm, name, "fast")
     assert np.array_equal(e.pressure(), g["p_cur"])
     assert np.array_equal(e.pressure_prev(), g["p_prev"])
@@ -325,36 +326,27 @@ def test_instability_is_reported_with_step(mm):
     assert 1 <= ei.value.step <= 400
 
 
-@pytest.mark.parametrize("ctas", ["16", "3"])
-def test_fast_boundary_few_ctas_regression(ctas, tmp_path):
-    """k_bnd with few CTAs (MM_BND_CTAS, read once per process): each CTA
-    pulls long mixed sequences of X/Y/Z-slab items through its stage ring.
-    Regression for a Z-slab tile whose rows past its box fall in a y damping
-    run: it read a zeta_y stage region its stage does not carry (out of the
-    ring's shared memory when the stage sat at the ring's end)."""
-    import subprocess
-    import sys
-    script = tmp_path / "few_ctas.py"
-    script.write_text(
-        "import sys, numpy as np\n"
-        f"sys.path.insert(0, {str(ROOT)!r})\n"
-        "import paper_2007_06048_b200 as mm\n"
-        "n, nd, src = (61, 47, 53), (9, 7, 11), (30, 23, 40)\n"
-        "g = mm.make_grid(n, (20.0, 15.0, 10.0), 4)\n"
-        "m = mm.random_model(g, seed=11)\n"
-        "w = mm.ricker(25.0, 1e-3, 60).samples\n"
-        "o = mm.EngineOptions(ndamping=nd, taper=True, free_surface=True)\n"
-        "e = {md: mm.AcousticCdEngine(g, (0, 0, 0), n, m.vp, o, 1e-3, m.vmax, mode=md)\n"
-        "     for md in ('fast', 'strict')}\n"
-        "for s in range(60):\n"
-        "    for x in e.values():\n"
-        "        x.step(float(w[s]), src)\n"
-        "assert np.array_equal(e['fast'].pressure(), e['strict'].pressure())\n"
-        "print('ok')\n")
-    env = dict(os.environ, MM_BND_CTAS=ctas)
-    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+@pytest.mark.parametrize("ctas", [16, 3])
+def test_fast_boundary_few_ctas_regression(mm, ctas):
+    """k_bnd (the two-pass path) with few CTAs (tuning bnd_ctas, read at
+    engine creation): each CTA pulls long mixed sequences of X/Y/Z-slab items
+    through its stage ring.  Regression for a Z-slab tile whose rows past its
+    box fall in a y damping run: it read a zeta_y stage region its stage does
+    not carry (out of the ring's shared memory when the stage sat at the
+    ring's end)."""
+    n, nd, src = (61, 47, 53), (9, 7, 11), (30, 23, 40)
+    g = mm.make_grid(n, (20.0, 15.0, 10.0), 4)
+    m = mm.random_model(g, seed=11)
+    w = mm.ricker(25.0, 1e-3, 60).samples
+    o = mm.EngineOptions(ndamping=nd, taper=True, free_surface=True)
+    with tuned(bnd_ctas=ctas, cpml_fused=0):
+        fast = mm.AcousticCdEngine(g, (0, 0, 0), n, m.vp, o, 1e-3, m.vmax, mode="fast")
+    strict = mm.AcousticCdEngine(g, (0, 0, 0), n, m.vp, o, 1e-3, m.vmax, mode="strict")
+    assert fast.cpml_path() == "two-pass"
+    for s in range(60):
+        for x in (fast, strict):
+            x.step(float(w[s]), src)
+    assert np.array_equal(fast.pressure(), strict.pressure())
 
 
 @pytest.mark.parametrize("n,nd,radius,fs", [
@@ -381,6 +373,9 @@ def test_tiny_and_degenerate_grids_vs_oracle(mm, oracle_port, n, nd, radius, fs)
                              taper=True, dt=1e-3, vmax=m.vmax)
     eng = {md: mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax, mode=md)
            for md in ("fast", "strict")}
+    with tuned(cpml_fused=0):
+        eng["fast-two-pass"] = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax,
+                                                   mode="fast")
     for s in range(15):
         ref.step(float(w[s]) * 1e3, src)
         for e in eng.values():
@@ -391,14 +386,14 @@ def test_tiny_and_degenerate_grids_vs_oracle(mm, oracle_port, n, nd, radius, fs)
         assert np.array_equal(e.pressure(), want), md
 
 
-@pytest.mark.parametrize("zslabs", ["0", "1", "2"])
+@pytest.mark.parametrize("zslabs", [-1, 0, 1, 2])
 @pytest.mark.parametrize("n,nd", [((5, 7, 9), (1, 2, 3)), ((9, 9, 9), (4, 4, 4)),
                                   ((24, 20, 7), (5, 4, 3))])
 def test_tiny_grids_every_zslab_schedule(mm, oracle_port, monkeypatch, zslabs, n, nd):
     """Free surface (low z layer inactive) with the high z run within R of the
     low Z slab: each Z-slab schedule (k_bnd tiles, k_zslab after k_inner,
-    k_zslab over whole columns) keeps the other run's dpsi_z out of it."""
-    monkeypatch.setenv("MM_ZSLABS", zslabs)
+    k_zslab over whole columns; -1: the default, k_cpml where it applies)
+    keeps the other run's dpsi_z out of it."""
     h = (20.0, 15.0, 10.0)
     grid = mm.make_grid(n, h, 4)
     m = mm.random_model(grid, seed=5)
@@ -406,10 +401,105 @@ def test_tiny_grids_every_zslab_schedule(mm, oracle_port, monkeypatch, zslabs, n
     src = tuple(x // 2 for x in n)
     ref = oracle_port.engine(n, m.vp, d=h, ndamping=nd, free_surface=True, taper=True,
                              dt=1e-3, vmax=m.vmax)
-    e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp,
-                            mm.EngineOptions(ndamping=nd, taper=True, free_surface=True),
-                            1e-3, m.vmax, mode="fast")
+    with tuned(zslabs=zslabs, cpml_fused=1 if zslabs < 0 else 0):
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp,
+                                mm.EngineOptions(ndamping=nd, taper=True, free_surface=True),
+                                1e-3, m.vmax, mode="fast")
     for s in range(15):
         ref.step(float(w[s]) * 1e3, src)
         e.step(float(w[s]) * 1e3, src)
     assert np.array_equal(e.pressure(), ref.pressure().reshape(grid.shape))
+
+
+# ---------------------------------------------------------------- k_cpml
+# The fused one-pass CPML kernel (fast_cpml.cuh) serves every layout whose
+# damping runs fit its 32-point tiles (fast mode's default path); these
+# layouts are chosen to exercise its tiling rules: misaligned high x runs,
+# partial middle tiles, rows owned by overlapping y tiles, nd = 0 axes, the
+# free surface (inactive low z run), r = 2, and z chunks next to the runs.
+CPML_CASES = [
+    ((70, 72, 60), (9, 10, 11), 4, False),
+    ((70, 72, 60), (9, 10, 11), 4, True),
+    ((61, 47, 53), (9, 7, 11), 4, True),
+    ((63, 66, 58), (9, 12, 10), 4, False),
+    ((80, 76, 70), (27, 27, 27), 4, False),
+    ((64, 64, 64), (0, 12, 12), 4, False),
+    ((64, 64, 64), (12, 0, 12), 4, True),
+    ((64, 64, 64), (12, 12, 0), 4, False),
+    ((50, 45, 40), (6, 8, 5), 2, False),
+    ((50, 45, 40), (6, 8, 5), 2, True),
+]
+
+
+@pytest.mark.parametrize("n,nd,radius,fs", CPML_CASES)
+def test_cpml_fused_bitwise_vs_oracle(mm, oracle_port, n, nd, radius, fs):
+    h = (20.0, 15.0, 10.0)
+    grid = mm.make_grid(n, h, radius)
+    m = mm.random_model(grid, seed=21)
+    steps = 30
+    w = mm.ricker(25.0, 1e-3, steps).samples
+    opts = mm.EngineOptions(ndamping=nd, taper=True, free_surface=fs)
+    src = tuple(x // 2 for x in n)
+    ref = oracle_port.engine(n, m.vp, d=h, radius=radius, ndamping=nd, free_surface=fs,
+                             taper=True, dt=1e-3, vmax=m.vmax)
+    e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax, mode="fast")
+    assert e.cpml_path() == "cpml"
+    for s in range(steps):
+        ref.step(float(w[s]) * 1e3, src)
+        e.step(float(w[s]) * 1e3, src)
+    want = ref.pressure().reshape(grid.shape)
+    got = e.pressure()
+    bad = int(np.count_nonzero(got != want))
+    assert bad == 0, f"{bad} points differ, rel L2 {rel_l2(got, want):.3e}"
+    assert np.array_equal(e.pressure_prev(), ref.pressure_prev().reshape(grid.shape))
+
+
+@pytest.mark.parametrize("chunk", [0, 5, 13, 1000])
+def test_cpml_fused_equals_two_pass_nd27(mm, chunk):
+    """128 x 120 x 136, nd 27 (the benchmark's damping) from a random field:
+    k_cpml (automatic and forced z-chunk lengths: chunk boundaries are pushed
+    out of the z runs' reach) == the two-pass kernels == strict, bitwise."""
+    n = (128, 120, 136)
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0), 4)
+    model = mm.default_layered_model(grid)
+    opts = mm.EngineOptions(ndamping=(27, 27, 27), taper=True)
+    rng = np.random.default_rng(3)
+    p0, p1 = grid.field(), grid.field()
+    grid.inner(p0)[...] = rng.standard_normal(n).astype(np.float32)
+    grid.inner(p1)[...] = rng.standard_normal(n).astype(np.float32)
+    dt = mm.cfl_dt(model, grid, 0.8)
+    with tuned(cpml_zt=chunk):
+        fused = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax)
+    with tuned(cpml_fused=0):
+        two = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax)
+    strict = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax,
+                                 mode="strict")
+    assert fused.cpml_path() == "cpml" and two.cpml_path() == "two-pass"
+    for e in (fused, two, strict):
+        e.set_state(p0, p1)
+        for s in range(12):
+            e.step(1.0, (64, 60, 68))
+    assert np.array_equal(fused.pressure(), strict.pressure())
+    assert np.array_equal(two.pressure(), strict.pressure())
+    assert np.array_equal(fused.pressure_prev(), strict.pressure_prev())
+
+
+def test_cpml_fused_device_loop_and_timing(mm):
+    """mm_cd_run (graph-captured rotation period) with k_cpml == host steps;
+    per-kernel timing names the step's kernels."""
+    n = (70, 72, 60)
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0), 4)
+    m = mm.random_model(grid, seed=4)
+    opts = mm.EngineOptions(ndamping=(9, 10, 11), taper=True)
+    w = mm.ricker(25.0, 1e-3, 40).samples * 1e3
+    a = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax)
+    b = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax)
+    a.run(w, (35, 36, 30), record=False)
+    b.kernel_timing(True)
+    for s in range(40):
+        b.step(float(w[s]), (35, 36, 30))
+    t = b.kernel_times()
+    b.kernel_timing(False)
+    assert np.array_equal(a.pressure(), b.pressure())
+    assert set(t) >= {"cpml", "inner", "epilogue"}, t
+    assert t["cpml"][1] == 40 and t["cpml"][0] > 0

@@ -7,6 +7,8 @@ velocities.  Also the reference's own VD property tests
 Propagator::AcousticIso, driver.cpp:122-128).
 """
 import numpy as np
+
+from paper_2007_06048_b200._lib import tuned
 import pytest
 
 from conftest import load_golden
@@ -186,16 +188,15 @@ def test_vd_cli_model_run(mm, tmp_path, oracle_ref):
 
 def test_vd_kernel_families_agree(mm, monkeypatch):
     """The TMA kernels (default) and the plain one-thread-per-point restatement
-    (MM_VD_SIMPLE=1, read at engine creation) are bit-identical."""
+    (tuning vd_simple=1, read at engine creation) are bit-identical."""
     n, r = (70, 66, 75), 4
     g, m = _model(mm, n, r, seed=11)
     opts = mm.EngineOptions(ndamping=(9, 10, 11), free_surface=True, taper=True)
     dt = 1e-3
     w = mm.integrate_wavelet(mm.ricker(25.0, dt, 40)).samples
     fast = mm.AcousticVdEngine(g, m, opts, dt)
-    monkeypatch.setenv("MM_VD_SIMPLE", "1")
-    plain = mm.AcousticVdEngine(g, m, opts, dt)
-    monkeypatch.delenv("MM_VD_SIMPLE")
+    with tuned(vd_simple=1):
+        plain = mm.AcousticVdEngine(g, m, opts, dt)
     for s in range(40):
         fast.step(float(w[s]) * 1e6, (20, 30, 40))
         plain.step(float(w[s]) * 1e6, (20, 30, 40))
@@ -206,42 +207,29 @@ def test_vd_kernel_families_agree(mm, monkeypatch):
     plain.close()
 
 
-@pytest.mark.parametrize("ctas", ["1", "7"])
-def test_vd_few_ctas(ctas, tmp_path):
-    """Long item sequences per CTA through the TMA rings (MM_VD_CTAS, read at
-    engine creation) on an odd free-surface grid: still bit-identical to the
-    plain kernels."""
-    import os
-    import subprocess
-    import sys
-    from conftest import ROOT
-    script = tmp_path / "vd_few.py"
-    script.write_text(
-        "import os, sys, numpy as np\n"
-        f"sys.path.insert(0, {str(ROOT)!r})\n"
-        "import paper_2007_06048_b200 as mm\n"
-        "n = (61, 47, 53)\n"
-        "g = mm.make_grid(n, (20.0, 15.0, 10.0), 4)\n"
-        "rng = np.random.default_rng(5)\n"
-        "vp, rho = g.field(), g.field()\n"
-        "g.inner(vp)[...] = rng.uniform(1500, 4500, n).astype(np.float32)\n"
-        "g.inner(rho)[...] = rng.uniform(1000, 2500, n).astype(np.float32)\n"
-        "m = mm.validate_model(mm.EarthModel(g, vp, rho=rho))\n"
-        "o = mm.EngineOptions(ndamping=(9, 7, 11), taper=True, free_surface=True)\n"
-        "w = mm.integrate_wavelet(mm.ricker(25.0, 1e-3, 40)).samples\n"
-        "fast = mm.AcousticVdEngine(g, m, o, 1e-3)\n"
-        "os.environ['MM_VD_SIMPLE'] = '1'\n"
-        "plain = mm.AcousticVdEngine(g, m, o, 1e-3)\n"
-        "for s in range(40):\n"
-        "    fast.step(float(w[s]) * 1e6, (30, 23, 26))\n"
-        "    plain.step(float(w[s]) * 1e6, (30, 23, 26))\n"
-        "assert np.array_equal(fast.pressure(), plain.pressure())\n"
-        "assert all(np.array_equal(fast.velocity(a), plain.velocity(a)) for a in range(3))\n"
-        "print('ok')\n")
-    env = dict(os.environ, MM_VD_CTAS=ctas)
-    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+@pytest.mark.parametrize("ctas", [1, 7])
+def test_vd_few_ctas(mm, ctas):
+    """Long item sequences per CTA through the TMA rings (tuning vd_ctas, read
+    at engine creation) on an odd free-surface grid: still bit-identical to
+    the plain kernels."""
+    n = (61, 47, 53)
+    g = mm.make_grid(n, (20.0, 15.0, 10.0), 4)
+    rng = np.random.default_rng(5)
+    vp, rho = g.field(), g.field()
+    g.inner(vp)[...] = rng.uniform(1500, 4500, n).astype(np.float32)
+    g.inner(rho)[...] = rng.uniform(1000, 2500, n).astype(np.float32)
+    m = mm.validate_model(mm.EarthModel(g, vp, rho=rho))
+    o = mm.EngineOptions(ndamping=(9, 7, 11), taper=True, free_surface=True)
+    w = mm.integrate_wavelet(mm.ricker(25.0, 1e-3, 40)).samples
+    with tuned(vd_ctas=ctas):
+        fast = mm.AcousticVdEngine(g, m, o, 1e-3)
+    with tuned(vd_simple=1):
+        plain = mm.AcousticVdEngine(g, m, o, 1e-3)
+    for s in range(40):
+        fast.step(float(w[s]) * 1e6, (30, 23, 26))
+        plain.step(float(w[s]) * 1e6, (30, 23, 26))
+    assert np.array_equal(fast.pressure(), plain.pressure())
+    assert all(np.array_equal(fast.velocity(a), plain.velocity(a)) for a in range(3))
 
 
 @pytest.mark.slow
@@ -257,9 +245,8 @@ def test_vd_large_grid_families_agree(mm, monkeypatch):
     p0 = g.field()
     g.inner(p0)[...] = rng.standard_normal(n).astype(np.float32)
     fast = mm.AcousticVdEngine(g, model, opts, 1e-3)
-    monkeypatch.setenv("MM_VD_SIMPLE", "1")
-    plain = mm.AcousticVdEngine(g, model, opts, 1e-3)
-    monkeypatch.delenv("MM_VD_SIMPLE")
+    with tuned(vd_simple=1):
+        plain = mm.AcousticVdEngine(g, model, opts, 1e-3)
     for e in (fast, plain):
         e.set_pressure(p0)
         for s in range(3):
