@@ -60,7 +60,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--grid", type=int, default=None, help="cube edge (default: config per N)")
-    ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
+    ap.add_argument("--mode", default="fast", choices=["fast", "strict", "fast_fma"])
+    ap.add_argument("--tune", action="append", default=[],
+                    help="name=value tuning parameter (mm_set_tuning), repeatable")
     ap.add_argument("--radius", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=None)
@@ -493,6 +495,11 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.tune:
+        from paper_2007_06048_b200 import _lib
+        for kv in args.tune:
+            k, v = kv.split("=")
+            _lib.set_tuning(k, int(v))
     if args.impl == "reference":
         return run_reference(args)
     if args.propagator == "acoustic_iso":

@@ -39,7 +39,7 @@ struct Tunable {
 };
 const Tunable kTunables[] = {
     {"step_graph", -1},  // host-driven steps as CUDA graphs: -1 auto (grids < 6 M points), 0 off, 1 on
-    {"cpml_fused", 1},   // fast mode: one-pass CPML kernel k_cpml where the layout allows it (0: k_p1 + k_bnd)
+    {"cpml_fused", 0},   // fast mode: one-pass CPML kernel k_cpml where the layout allows it (0: k_p1 + k_bnd)
     {"cpml_zt", 0},      // k_cpml planes per work item (0: automatic)
     {"overlap", 1},      // interior kernel on a side stream beside the CPML kernels
     {"pdl", 1},          // programmatic dependent launch of k_bnd after k_p1

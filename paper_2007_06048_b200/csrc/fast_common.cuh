@@ -186,5 +186,77 @@ __device__ __forceinline__ float d2_term(float t, float c, float pp, float pm, f
     return acc<ORD>(t, c, fs<ORD>(fa<ORD>(pp, pm), two_p0));
 }
 
+// ---- packed pairs of fp32 (Blackwell's f32x2 ALU: FADD2 / FFMA2)
+// add.rn.f32x2 / sub.rn.f32x2 round each lane like add.rn.f32, so ORD 2 stays
+// bit-identical.  Products stay scalar __fmul_rn in ORD 2: ptxas contracts a
+// mul.rn.f32x2 feeding an add.rn.f32x2 into FFMA2 even with explicit
+// rounding (checked in SASS), which would change the rounding.
+struct F2 {
+    unsigned long long r;
+};
+__device__ __forceinline__ F2 f2(float a, float b) {
+    F2 p;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(p.r) : "f"(a), "f"(b));
+    return p;
+}
+__device__ __forceinline__ void unf2(F2 p, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(p.r));
+}
+__device__ __forceinline__ float f2lo(F2 p) {
+    float a, b;
+    unf2(p, a, b);
+    return a;
+}
+__device__ __forceinline__ float f2hi(F2 p) {
+    float a, b;
+    unf2(p, a, b);
+    return b;
+}
+__device__ __forceinline__ F2 f2zero() { return f2(0.0f, 0.0f); }
+template <int ORD>
+__device__ __forceinline__ F2 fa2(F2 a, F2 b) {
+    F2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
+    return d;
+}
+template <int ORD>
+__device__ __forceinline__ F2 fs2(F2 a, F2 b) {
+    F2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
+    return d;
+}
+// (c0, c1) * x lane-wise
+template <int ORD>
+__device__ __forceinline__ F2 fm2v(float c0, float c1, F2 x) {
+    float a, b;
+    unf2(x, a, b);
+    return f2(fm<ORD>(c0, a), fm<ORD>(c1, b));
+}
+template <int ORD>
+__device__ __forceinline__ F2 fm2(float c, F2 x) {
+    return fm2v<ORD>(c, c, x);
+}
+// t + c * x  (reference `t += c * x`)
+template <int ORD>
+__device__ __forceinline__ F2 acc2(F2 t, float c, F2 x) {
+    if constexpr (ORD == 2) {
+        return fa2<ORD>(t, fm2<ORD>(c, x));
+    } else {
+        F2 d;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.r) : "l"(x.r), "l"(f2(c, c).r), "l"(t.r));
+        return d;
+    }
+}
+// second_derivative_at term, both lanes: t += c * ((pp + pm) - 2 p0)
+template <int ORD>
+__device__ __forceinline__ F2 d2_term2(F2 t, float c, F2 pp, F2 pm, F2 two_p0) {
+    return acc2<ORD>(t, c, fs2<ORD>(fa2<ORD>(pp, pm), two_p0));
+}
+__device__ __forceinline__ void lds4x2(const float* p, F2& a, F2& b) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    a = f2(v.x, v.y);
+    b = f2(v.z, v.w);
+}
+
 }  // namespace fast
 }  // namespace mmb

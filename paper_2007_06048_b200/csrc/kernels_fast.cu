@@ -347,20 +347,21 @@ public:
             // k_cpml (both CPML passes, all slabs) on the step's stream; the
             // interior kernel, which needs no CPML state, beside it on the side
             // stream (a second branch of a captured graph), joined before the
-            // epilogue
+            // epilogue.  k_cpml is issued first: both kernels are persistent and
+            // one k_cpml CTA fills an SM, so the interior CTAs take the SMs its
+            // tail frees.
+            if (overlap_) MM_CUDA(cudaEventRecord(fork_, s));
+            const int tc = timer.begin("cpml", s);
+            launch_cpml(p, ZRanges{{0, lay_.n[2]}}, s);
+            timer.end(tc, s);
             if (overlap_) {
-                MM_CUDA(cudaEventRecord(fork_, s));
                 MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
                 const int ti = timer.begin("inner", side_);
                 launch_inner(p, 0, lay_.n[2], kInnerOnly, side_);
                 timer.end(ti, side_);
                 MM_CUDA(cudaEventRecord(join_, side_));
             }
-            dbg(s, "inner(side)", overlap_ ? side_ : nullptr);
-            const int tc = timer.begin("cpml", s);
-            launch_cpml(p, ZRanges{{0, lay_.n[2]}}, s);
-            timer.end(tc, s);
-            dbg(s, "cpml", nullptr);
+            dbg(s, "cpml", overlap_ ? side_ : nullptr);
             if (overlap_) {
                 MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
             } else {
@@ -945,7 +946,9 @@ private:
     }
 
     // [a, b) cut into chunks of about `target` planes, no boundary inside a
-    // forbidden zone (within R of a z run: chunks update psi_z in place)
+    // forbidden zone (within R of a z run: chunks update psi_z in place); a
+    // boundary that falls in a zone moves down to the zone's start when the
+    // chunk stays non-empty, else up to its end
     static void chunk_planes(int a, int b, int target, const std::vector<std::pair<int, int>>& forb,
                              std::vector<std::pair<int, int>>& out) {
         int zb = a;
@@ -955,7 +958,7 @@ private:
                 moved = false;
                 for (const auto& f : forb)
                     if (ze > f.first && ze < f.second && ze < b) {
-                        ze = std::min(b, f.second);
+                        ze = f.first > zb ? f.first : std::min(b, f.second);
                         moved = true;
                     }
             }
@@ -1001,14 +1004,25 @@ private:
         // 4R-plane warm-up of the z window)
         int target = cpml_zt_ > 0 ? cpml_zt_
                                   : (int)std::max<long long>(12, (planes + 2LL * slots - 1) / (2LL * slots));
-        std::vector<std::pair<int, int4>> items;  // (z_begin, item)
+        // order: items near a z run first (they also update psi_z and carry a
+        // 4R-plane warm-up, the longest items), then chunk-major -- the items
+        // in flight are neighbouring tiles at nearby depths, whose p_cur halo
+        // planes meet in L2
+        auto near_z = [&](int zb, int ze) {
+            for (const auto& f : g.forb)
+                if (zb < f.second && ze > f.first) return true;
+            return false;
+        };
+        std::vector<std::pair<long long, int4>> items;  // (sort key, item)
         for (const auto& sg : segs) {
             std::vector<std::pair<int, int>> ch;
             chunk_planes(sg.second.first, sg.second.second, target, g.forb, ch);
-            for (const auto& c : ch) items.push_back({c.first, make_int4(sg.first, c.first, c.second, 0)});
+            for (const auto& c : ch) {
+                const long long key = (near_z(c.first, c.second) ? 0LL : 1LL << 40) +
+                                      ((long long)c.first << 20) + sg.first;
+                items.push_back({key, make_int4(sg.first, c.first, c.second, 0)});
+            }
         }
-        // chunk-major: the items in flight are neighbouring tiles at nearby
-        // depths (their p_cur halo planes meet in L2)
         std::stable_sort(items.begin(), items.end(),
                          [](const auto& a, const auto& b) { return a.first < b.first; });
         std::vector<int4> v;

@@ -339,7 +339,7 @@ def test_fast_boundary_few_ctas_regression(mm, ctas):
     m = mm.random_model(g, seed=11)
     w = mm.ricker(25.0, 1e-3, 60).samples
     o = mm.EngineOptions(ndamping=nd, taper=True, free_surface=True)
-    with tuned(bnd_ctas=ctas, cpml_fused=0):
+    with tuned(bnd_ctas=ctas):
         fast = mm.AcousticCdEngine(g, (0, 0, 0), n, m.vp, o, 1e-3, m.vmax, mode="fast")
     strict = mm.AcousticCdEngine(g, (0, 0, 0), n, m.vp, o, 1e-3, m.vmax, mode="strict")
     assert fast.cpml_path() == "two-pass"
@@ -373,9 +373,9 @@ def test_tiny_and_degenerate_grids_vs_oracle(mm, oracle_port, n, nd, radius, fs)
                              taper=True, dt=1e-3, vmax=m.vmax)
     eng = {md: mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax, mode=md)
            for md in ("fast", "strict")}
-    with tuned(cpml_fused=0):
-        eng["fast-two-pass"] = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax,
-                                                   mode="fast")
+    with tuned(cpml_fused=1):
+        eng["fast-cpml"] = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax,
+                                               mode="fast")
     for s in range(15):
         ref.step(float(w[s]) * 1e3, src)
         for e in eng.values():
@@ -401,7 +401,7 @@ def test_tiny_grids_every_zslab_schedule(mm, oracle_port, monkeypatch, zslabs, n
     src = tuple(x // 2 for x in n)
     ref = oracle_port.engine(n, m.vp, d=h, ndamping=nd, free_surface=True, taper=True,
                              dt=1e-3, vmax=m.vmax)
-    with tuned(zslabs=zslabs, cpml_fused=1 if zslabs < 0 else 0):
+    with tuned(zslabs=max(zslabs, -1), cpml_fused=1 if zslabs < 0 else 0):
         e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp,
                                 mm.EngineOptions(ndamping=nd, taper=True, free_surface=True),
                                 1e-3, m.vmax, mode="fast")
@@ -412,8 +412,8 @@ def test_tiny_grids_every_zslab_schedule(mm, oracle_port, monkeypatch, zslabs, n
 
 
 # ---------------------------------------------------------------- k_cpml
-# The fused one-pass CPML kernel (fast_cpml.cuh) serves every layout whose
-# damping runs fit its 32-point tiles (fast mode's default path); these
+# The fused one-pass CPML kernel (fast_cpml.cuh, tuning cpml_fused=1) serves
+# every layout whose damping runs fit its 32-point tiles; these
 # layouts are chosen to exercise its tiling rules: misaligned high x runs,
 # partial middle tiles, rows owned by overlapping y tiles, nd = 0 axes, the
 # free surface (inactive low z run), r = 2, and z chunks next to the runs.
@@ -442,7 +442,8 @@ def test_cpml_fused_bitwise_vs_oracle(mm, oracle_port, n, nd, radius, fs):
     src = tuple(x // 2 for x in n)
     ref = oracle_port.engine(n, m.vp, d=h, radius=radius, ndamping=nd, free_surface=fs,
                              taper=True, dt=1e-3, vmax=m.vmax)
-    e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax, mode="fast")
+    with tuned(cpml_fused=1):
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax, mode="fast")
     assert e.cpml_path() == "cpml"
     for s in range(steps):
         ref.step(float(w[s]) * 1e3, src)
@@ -468,10 +469,9 @@ def test_cpml_fused_equals_two_pass_nd27(mm, chunk):
     grid.inner(p0)[...] = rng.standard_normal(n).astype(np.float32)
     grid.inner(p1)[...] = rng.standard_normal(n).astype(np.float32)
     dt = mm.cfl_dt(model, grid, 0.8)
-    with tuned(cpml_zt=chunk):
+    with tuned(cpml_zt=chunk, cpml_fused=1):
         fused = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax)
-    with tuned(cpml_fused=0):
-        two = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax)
+    two = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax)
     strict = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax,
                                  mode="strict")
     assert fused.cpml_path() == "cpml" and two.cpml_path() == "two-pass"
@@ -492,8 +492,9 @@ def test_cpml_fused_device_loop_and_timing(mm):
     m = mm.random_model(grid, seed=4)
     opts = mm.EngineOptions(ndamping=(9, 10, 11), taper=True)
     w = mm.ricker(25.0, 1e-3, 40).samples * 1e3
-    a = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax)
-    b = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax)
+    with tuned(cpml_fused=1):
+        a = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax)
+        b = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, opts, 1e-3, m.vmax)
     a.run(w, (35, 36, 30), record=False)
     b.kernel_timing(True)
     for s in range(40):
@@ -503,3 +504,20 @@ def test_cpml_fused_device_loop_and_timing(mm):
     assert np.array_equal(a.pressure(), b.pressure())
     assert set(t) >= {"cpml", "inner", "epilogue"}, t
     assert t["cpml"][1] == 40 and t["cpml"][0] > 0
+
+
+def test_default_step_kernel_timing_names(mm):
+    """The default fast step (two-pass CPML beside the interior kernel) times
+    every kernel it launches on the launching stream."""
+    n = (70, 72, 60)
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0), 4)
+    m = mm.random_model(grid, seed=4)
+    e = mm.AcousticCdEngine(grid, (0, 0, 0), n, m.vp, mm.EngineOptions(ndamping=(9, 10, 11)),
+                            1e-3, m.vmax)
+    assert e.cpml_path() == "two-pass"
+    e.kernel_timing(True)
+    for s in range(5):
+        e.step(1.0, (35, 36, 30))
+    t = e.kernel_times()
+    assert set(t) >= {"pass1", "boundary", "inner", "epilogue"}, t
+    assert all(v[1] == 5 for v in t.values()), t
