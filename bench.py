@@ -2,8 +2,16 @@
 """bench.py -- Gpoints/s of the acoustic_iso_cd propagator on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--grid 240] [--mode fast|strict] [--radius 4]
-                    [--propagator acoustic_iso_cd|acoustic_iso]
+                    [--grid 240] [--mode fast|strict|fast_fma] [--radius 4]
+                    [--scaling weak|strong] [--propagator acoustic_iso_cd|acoustic_iso]
+                    [--tune name=value ...]
+
+N > 1 (torchrun, or spawned by bench.py itself when WORLD_SIZE is unset): one
+rank per GPU through the C++ z-slab group (mm_cd_group_run: NCCL halo planes
+overlapped with the interior), weak scaling at 240^3 per GPU by default;
+--scaling strong --grid 512|1000 fixes the global grid (BASELINE configs[2],
+configs[3]) and adds the parallel efficiency of bench.cpp:130-145 against one
+GPU on the same grid.
 
 A "step" is one time step of the propagator over the whole grid (the
 reference's eng.step(), driver.cpp:104-106).  Workload at N=1: BASELINE.json
@@ -66,6 +74,11 @@ def parse():
     ap.add_argument("--radius", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=None)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = 240^3 per GPU (grid 240 x 240 x 240 N); strong = the "
+                         "--grid^3 global grid (default 1000) cut into N z-slabs")
+    ap.add_argument("--no-efficiency", dest="efficiency", action="store_false",
+                    help="strong scaling: skip the one-GPU baseline on the same grid")
     ap.add_argument("--propagator", default="acoustic_iso_cd",
                     choices=["acoustic_iso_cd", "acoustic_iso"],
                     help="acoustic_iso: the variable-density engine (SURVEY 8(f) row 4)")
@@ -172,7 +185,11 @@ def cpu_sample_steps(n, requested):
 # ------------------------------------------------------------------ our arm
 def workload_grid(args, world):
     """BASELINE configs[1] per GPU: 240^3 at N = 1; weak scaling at N > 1 grows
-    z, 240 x 240 x 240 N (the multi-GPU leg in dist.bench_rank uses the same)."""
+    z, 240 x 240 x 240 N; strong scaling keeps --grid^3 (default 1000^3) for
+    every N (the multi-GPU leg in dist.bench_rank uses the same)."""
+    if args.scaling == "strong":
+        edge = args.grid or 1000
+        return (edge, edge, edge)
     edge = args.grid or 240
     return (edge, edge, edge * world)
 
@@ -182,6 +199,8 @@ def run_ours(args):
     if world > 1 or os.environ.get("MM_BENCH_ZSLAB") == "1":  # (world 1: the z-slab leg alone)
         from paper_2007_06048_b200 import dist as mmdist
         return mmdist.bench_rank(args, rank, world, local)
+    if args.scaling == "strong" and args.grid is None:
+        args.grid = 1000  # BASELINE configs[3] at N = 1 (the strong-scaling baseline)
     import torch
     import paper_2007_06048_b200 as mm
     from paper_2007_06048_b200 import _lib
@@ -286,6 +305,8 @@ def run_ours(args):
                       "achieved_gbs": (round(kb[k] / (kms[k] * 1e-3) / 1e9, 1)
                                        if k in kb else None)} for k in kms}
 
+    from paper_2007_06048_b200.scaling import count_stencil_cost
+    cost = count_stencil_cost("acoustic_iso_cd", r)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -295,6 +316,8 @@ def run_ours(args):
                                f"{nrec} surface receivers (BASELINE configs[1])",
                    "grid": list(n), "radius": r, "ndamping": list(nd), "mode": args.mode,
                    "cpml_path": eng.cpml_path(),
+                   "flops_per_point": cost.flops_per_point,
+                   "arithmetic_intensity": round(cost.arithmetic_intensity, 4),
                    "l2": "working set (3 p fields + c + CPML) > 126 MB L2; no flush"},
         "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": 4,
                 "d2h_bytes_per_step": 4 * nrec},
@@ -493,8 +516,36 @@ def run_reference(args):
     return 0
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` started without torchrun: launch N ranks (one per
+    GPU) through torch.distributed.run on this node and relay their output."""
+    import socket
+    try:
+        import torch
+        have = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        have = 0
+    if args.impl == "ours" and have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but {have} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if args.gpus > 1:
+        # NCCL init lines (ranks, transports) on stderr; stdout keeps the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.tune:
         from paper_2007_06048_b200 import _lib
         for kv in args.tune:

@@ -224,6 +224,50 @@ int mm_cd_update_planes(mm_cd_engine* e, int z_lo, int z_hi);
 int mm_cd_update_plane_ranges(mm_cd_engine* e, const int* ranges, int n);
 
 /* ------------------------------------------------------------------------
+ * Multi-GPU z-slab group (ref: run_distributed_rank, dist.cpp:144-267, with
+ * Cartesian dims {1, 1, P}; exchange_halos, dist.cpp:92-115).  One process
+ * (rank) per GPU; the host runtime shares one NCCL unique id between the
+ * ranks (e.g. a torch.distributed broadcast) and every rank creates its
+ * group with it.  NCCL is loaded at run time (libnccl.so.2).
+ * --------------------------------------------------------------------- */
+typedef struct mm_cd_group mm_cd_group;
+
+/* ncclGetUniqueId: 128 bytes for mm_cd_group_create (made by rank 0). */
+int mm_nccl_get_unique_id(unsigned char id[128]);
+/* ref: dist.cpp:119-132 validate_cuts for z cuts[world+1] (0 = cuts[0] <
+ * ... < cuts[world] = nz): interior cuts at least ndamping_z + radius from
+ * both faces, slabs at least radius planes thick.  MM_ECONFIG otherwise. */
+int mm_zslab_validate_cuts(const int* cuts, int world, int nz, int ndamping_z, int radius);
+/* One rank's slab [cuts[rank], cuts[rank+1]) of the global grid: its engine
+ * (vp_local: the ghosted z-fastest slice of the global model, the
+ * reference's vp_local, dist.cpp:171-180), the halo plan and the NCCL
+ * communicator (ncclCommInitRank: a collective over all ranks).  nccl_id may
+ * be NULL for world == 1. */
+int mm_cd_group_create(const mm_grid* global, const int* cuts, int world, int rank,
+                       const unsigned char nccl_id[128], const float* vp_local,
+                       const mm_engine_options* opts, float dt, double vmax, int device, int mode,
+                       mm_cd_group** out);
+int mm_cd_group_destroy(mm_cd_group* g);
+/* The rank's slab engine (owned by the group): receivers, pressure, traces,
+ * stream.  Its local z = global z - z0. */
+int mm_cd_group_engine(mm_cd_group* g, mm_cd_engine** e);
+int mm_cd_group_slab(mm_cd_group* g, int* z0, int* nz);
+/* One step on every rank (ref: exchange_halos + eng.step, dist.cpp:212-215):
+ * CPML pass 1 -> the r planes next to each cut -> NCCL send/recv of those
+ * planes into the neighbours' ghost planes on a communication stream,
+ * overlapped with the interior planes -> join -> source (global coordinates;
+ * the owning rank injects), free surface (rank 0), rotation.  Asynchronous
+ * on the engine stream. */
+int mm_cd_group_step(mm_cd_group* g, float amp, const int* src_global);
+/* nsteps group steps with device amplitudes, receiver recording into columns
+ * [first_sample, ...) when record != 0 (the rank's own receivers), and the
+ * reference's per-rank finiteness check of the slab centre every step
+ * (dist.cpp:222-224): MM_EINSTABILITY with the first failing step.
+ * *device_ms: device time of this rank's loop. */
+int mm_cd_group_run(mm_cd_group* g, const float* amps, int nsteps, const int* src_global,
+                    int record, int first_sample, float* device_ms);
+
+/* ------------------------------------------------------------------------
  * Driver (ref: driver.cpp:83-144 run(), acoustic_iso_cd only)
  * --------------------------------------------------------------------- */
 typedef struct mm_sim_config {

@@ -137,6 +137,16 @@ SIGNATURES = {
     "mm_cd_next_halo_planes": [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_size_t)],
     "mm_cd_update_planes": [_P, C.c_int, C.c_int],
     "mm_cd_update_plane_ranges": [_P, C.POINTER(C.c_int), C.c_int],
+    "mm_nccl_get_unique_id": [C.c_void_p],
+    "mm_zslab_validate_cuts": [_ip, C.c_int, C.c_int, C.c_int, C.c_int],
+    "mm_cd_group_create": [C.POINTER(mm_grid), _ip, C.c_int, C.c_int, C.c_void_p, _fp,
+                           C.POINTER(mm_engine_options), C.c_float, C.c_double, C.c_int, C.c_int,
+                           C.POINTER(_P)],
+    "mm_cd_group_destroy": [_P],
+    "mm_cd_group_engine": [_P, C.POINTER(_P)],
+    "mm_cd_group_slab": [_P, _ip, _ip],
+    "mm_cd_group_step": [_P, C.c_float, _ip],
+    "mm_cd_group_run": [_P, _fp, C.c_int, _ip, C.c_int, C.c_int, _fp],
     "mm_sim_config_default": [C.POINTER(mm_sim_config)],
     "mm_run": [C.POINTER(mm_sim_config), _fp, C.c_int, C.c_int, _fp, C.POINTER(mm_run_report)],
     # acoustic_iso (variable density)

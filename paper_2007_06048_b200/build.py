@@ -79,7 +79,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
     newest = max(o.stat().st_mtime for o in objs)
     if force or not lib.exists() or lib.stat().st_mtime < newest:
         tmp = lib.with_suffix(".so.tmp")
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread"]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")

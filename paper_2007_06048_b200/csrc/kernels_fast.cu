@@ -341,6 +341,24 @@ public:
         launch_boundary(p, zr, s);
     }
 
+    void update_overlap(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) override {
+        const bool fc = fast_cpml(p);
+        if (!fc || zmode_ != 0 || !overlap_) {
+            update(p, 0, z_lo, z_hi, s);
+            return;
+        }
+        MM_CUDA(cudaEventRecord(fork_, s));
+        MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+        const int ti = timer.begin("inner", side_);
+        launch_inner(p, z_lo, z_hi, kInnerOnly, side_);
+        timer.end(ti, side_);
+        MM_CUDA(cudaEventRecord(join_, side_));
+        const int tb = timer.begin("boundary", s);
+        launch_boundary(p, z_lo, z_hi, s);
+        timer.end(tb, s);
+        MM_CUDA(cudaStreamWaitEvent(s, join_, 0));
+    }
+
     void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
               const int* step_dev, cudaStream_t s) override {
         if (use_cpml(p)) {

@@ -229,8 +229,9 @@ __global__ void k_epilogue(Epilogue e) {
         e.rec.traces[(long long)step * e.rec.nrec + r] = v;
         // ref: driver.cpp:68-71,108 check_finite(rec.at(0, n), n + 1)
         if (r == 0 && !isfinite(v) && e.rec.bad_step) atomicMin(e.rec.bad_step, step + 1);
-    } else if (t == nfs && e.rec.nrec == 0 && e.check_off >= 0 && e.rec.bad_step) {
-        // no recording: the same per-step check on one point (receiver 0 or the source)
+    } else if (t == nfs + e.rec.nrec && e.check_off >= 0 && e.rec.bad_step) {
+        // per-step finiteness check of one more point: receiver 0 or the source
+        // without recording (mm_cd_run), a slab's centre (dist.cpp:222-224)
         const bool on_surface = e.fs && e.check_off / L.plane == L.r;
         const float v = on_surface ? 0.0f : value(e.check_off);
         if (!isfinite(v)) atomicMin(e.rec.bad_step, step + 1);
@@ -349,7 +350,7 @@ void launch_step_counter(int* step_dev, cudaStream_t s) {
 
 void launch_epilogue(const Epilogue& ep, cudaStream_t s) {
     const long long nfs = ep.fs ? (long long)(ep.lay.n[0] + 2 * ep.lay.r) * ep.lay.ey : 0;
-    const long long work = nfs + std::max<long long>(ep.rec.nrec, ep.check_off >= 0 ? 1 : 0);
+    const long long work = nfs + ep.rec.nrec + (ep.check_off >= 0 ? 1 : 0);
     if (work == 0 && ep.src_off < 0 && !ep.count) return;
     const int blocks = (int)std::max<long long>((work + 255) / 256, 1);
     k_epilogue<<<blocks, 256, 0, s>>>(ep);

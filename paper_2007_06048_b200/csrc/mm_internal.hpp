@@ -260,7 +260,7 @@ struct Epilogue {
     bool fs;               // free surface at local z = 0
     Layout lay;
     RecParams rec;         // nrec = 0: no sampling (rec.p is ignored: p)
-    long long check_off;   // >= 0 and rec.nrec == 0: finiteness check of this point into rec.bad_step
+    long long check_off;   // >= 0: finiteness check of this point into rec.bad_step
     int* done;             // block ticket (zero between launches)
 };
 

@@ -16,11 +16,13 @@ B200 design:
   overlapped with the interior planes -> join -> source / free surface ->
   rotate.  The exchanged planes become the neighbours' p_cur ghosts, exactly
   what the reference's exchange_halos(p_cur) produces before the next step.
-The "simple" schedule (exchange p_cur, then step) is the reference's own
-order and is what the CPU (gloo) tests drive.
-
-Transports: ``TorchTransport`` (torch.distributed, NCCL on GPUs, gloo on CPU)
-and ``LocalTransport`` (all ranks in one process; device-to-device copies).
+The GPU ranks run that schedule in C++ (mm_cd_group_*, csrc/group.cu, NCCL
+inside); this module plans the cuts, shares the NCCL id and drives the bench.
+``ZSlabRank`` / ``step_local`` restate the same schedule in Python over the
+plane-range C ABI for the single-GPU emulation test (all ranks in one
+process, device-to-device halo copies); the "simple" schedule (exchange p_cur,
+then step) is the reference's own order, which the CPU (gloo) tests drive
+with ``TorchTransport``.
 """
 from __future__ import annotations
 
@@ -192,7 +194,10 @@ def halo_pairs(info: SlabInfo):
 
 # --------------------------------------------------------------- GPU rank
 class ZSlabRank:
-    """One rank of the GPU z-slab run (wraps an AcousticCdEngine)."""
+    """Python restatement of the group schedule (csrc/group.cu) for one slab
+    engine, over the plane-range C ABI: the single-GPU emulation test drives
+    several of them in one process (step_local), halo planes moved with
+    device-to-device copies where the C++ group uses NCCL."""
 
     def __init__(self, engine, info: SlabInfo, transport, src_global=None):
         self.e = engine
@@ -216,22 +221,6 @@ class ZSlabRank:
 
             v = self._views[key] = torch.as_tensor(_A(), device=f"cuda:{self.e.device}")
         return v
-
-    def exchange_current(self):
-        """Reference order: exchange p_cur ghosts (dist.cpp:213-214)."""
-        sends, recvs = [], []
-        for peer, side in halo_pairs(self.info):
-            sends.append((peer, self._view(side, 0, False)))
-            recvs.append((peer, self._view(side, 1, False)))
-        return self.t.exchange(sends, recvs)
-
-    def step_simple(self, amp: float):
-        import torch
-        ext = torch.cuda.ExternalStream(self.e.stream_handle(), device=self.e.device)
-        with torch.cuda.stream(ext):
-            works = self.exchange_current()
-            self.t.wait(works)
-        self.e.step(amp, self.src_local)
 
     # ---- overlap schedule, in phases (a LocalTransport driver interleaves
     # the phases of several ranks; step_overlap runs them back to back)
@@ -282,18 +271,6 @@ class ZSlabRank:
         self.e.apply_free_surface()
         self.e.rotate()
 
-    def step_overlap(self, amp: float):
-        """edges -> NCCL(edges) || interior -> join -> finish (see module doc)."""
-        import torch
-        ext = torch.cuda.ExternalStream(self.e.stream_handle(), device=self.e.device)
-        with torch.cuda.stream(ext):
-            self.phase_edges(amp)
-            sends, recvs = self.halo_messages()
-            works = self.t.exchange(sends, recvs)  # NCCL waits for the edges
-            self.phase_interior()                  # concurrent with the transfer
-            self.t.wait(works)                     # engine stream waits for NCCL
-            self.phase_finish(amp)
-
 
 def step_local(ranks: Sequence["ZSlabRank"], amp: float):
     """All ranks in one process (LocalTransport semantics): the overlap
@@ -319,79 +296,99 @@ def step_local(ranks: Sequence["ZSlabRank"], amp: float):
         rk.phase_finish(amp)
 
 
-def run_zslab(mm, config, vp_global: np.ndarray, info: SlabInfo, transport, *, device=0,
-              mode="fast", schedule="overlap", nsteps=None, timed=False):
-    """Distributed acoustic_iso_cd run (ref: dist.cpp:144-267) on one rank.
+def layered_slice(n: Sequence[int], z0: int, nz: int, radius: int) -> np.ndarray:
+    """The rank's ghosted slice [z0 - r, z0 + nz + r) of the global
+    default_layered_model (model.cpp:63-77: vp 1500 for k < n_z/2, 4500 below;
+    ghosts replicate the edge values), built without the global volume
+    (1000^3 would be 4 GB per rank)."""
+    r = radius
+    k = np.clip(np.arange(z0 - r, z0 + nz + r), 0, n[2] - 1)
+    col = np.where(k < n[2] // 2, 1500.0, 4500.0).astype(np.float32)
+    return np.ascontiguousarray(np.broadcast_to(col, (n[0] + 2 * r, n[1] + 2 * r, nz + 2 * r)))
 
-    Returns dict(traces on rank 0 for receivers owned by rank 0 -- all of them
-    for legal cuts, since the receiver plane k = nd_z lies below the first cut),
-    dt, device_seconds)."""
-    import torch
+
+def share_nccl_id(rank: int) -> bytes:
+    """Rank 0's NCCL unique id, broadcast over the torch.distributed process
+    group (the host plumbing; the halo traffic itself is the C++ group's)."""
+    import torch.distributed as dist
+    from .propagator import nccl_unique_id
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def run_zslab(mm, config, vp_global: Optional[np.ndarray], info: SlabInfo, *, device=0,
+              mode="fast", nsteps=None, nccl_id: Optional[bytes] = None, vp_local=None):
+    """Distributed acoustic_iso_cd run (ref: run_distributed_rank,
+    dist.cpp:144-267) on one rank, through the C++ group (mm_cd_group_*: NCCL
+    halo exchange overlapped with the interior, per-rank finiteness check).
+
+    Returns dict(traces of the receivers this rank owns -- all of them on
+    rank 0 for legal cuts, since the receiver plane k = nd_z lies below the
+    first cut --, dt, device_seconds, group)."""
+    from .propagator import ZSlabGroup
     n = tuple(config.ngrid)
     r = config.stencil_radius
     grid = mm.make_grid(n, config.dgrid, r)
-    model = mm.EarthModel(grid, vp_global)
-    model = mm.validate_model(model)
-    dt = mm.cfl_dt(model, grid, config.cfl)
-    w = mm.ricker(config.fmax, dt, config.nsteps).samples
-    lgrid = mm.make_grid((n[0], n[1], info.nz), config.dgrid, r)
-    vp_loc = local_vp(model.vp, r, info.z0, info.nz)
+    if vp_local is None:
+        model = mm.validate_model(mm.EarthModel(grid, vp_global))
+        vmax = model.vmax
+        vp_global = model.vp
+    else:
+        vmax = float(vp_local.max())
+    dt = cfl_dt_vmax(vmax, grid, config.cfl)
+    steps = config.nsteps if nsteps is None else nsteps
+    w = mm.ricker(config.fmax, dt, max(steps, 1)).samples
     opts = mm.EngineOptions(ndamping=tuple(config.ndamping), fmax=config.fmax,
                             r_target=config.r_target, free_surface=config.free_surface,
                             taper=config.taper, ntaper=tuple(config.ntaper))
-    eng = mm.AcousticCdEngine(lgrid, (0, 0, info.z0), n, vp_loc, opts, float(np.float32(dt)),
-                              model.vmax, device=device, mode=mode)
+    grp = ZSlabGroup(grid, info.cuts, info.rank, vp_global, opts, float(np.float32(dt)), vmax,
+                     nccl_id=nccl_id, device=device, mode=mode, vp_local=vp_local)
     src = config.source_loc if config.source_loc is not None else tuple(x // 2 for x in n)
-    rk = ZSlabRank(eng, info, transport, src)
-    geo = mm.default_receivers(grid, config.ndamping, config.receiver_increment)
     k_rec = config.ndamping[2]
     owns_rec = info.z0 <= k_rec < info.z0 + info.nz
-    steps = config.nsteps if nsteps is None else nsteps
     if owns_rec:
-        rec = geo.receivers.copy()
-        rec[:, 2] -= info.z0
-        eng.set_receivers(rec, steps)
-    # initial p_cur ghosts (all zero unless seeded): the overlap schedule
-    # exchanges p_next after every step, so one exchange up front suffices
-    torch.cuda.synchronize()
-    transport.barrier()
-    t0 = time.perf_counter()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ext = torch.cuda.ExternalStream(eng.stream_handle(), device=device)
-    ev0.record(ext)
-    for s in range(steps):
-        if schedule == "overlap":
-            rk.step_overlap(float(w[s]))
-        else:
-            rk.step_simple(float(w[s]))
-        if owns_rec:
-            eng.record(s)
-    ev1.record(ext)
-    eng.synchronize()
-    torch.cuda.synchronize()
-    dev_s = ev0.elapsed_time(ev1) * 1e-3
-    transport.barrier()
-    out = {"dt": dt, "device_seconds": dev_s, "wall_seconds": time.perf_counter() - t0,
-           "engine": eng, "owns_receivers": owns_rec}
+        grp.engine.set_receivers(_receivers_local(mm, grid, config, info), steps)
+    ms = grp.run(w[:steps], src, record=owns_rec) if steps > 0 else 0.0
+    out = {"dt": dt, "device_seconds": ms * 1e-3, "group": grp, "owns_receivers": owns_rec}
     if owns_rec:
-        out["traces"] = eng.traces(steps)
+        out["traces"] = grp.engine.traces(steps)
     return out
+
+
+def cfl_dt_vmax(vmax: float, grid, cfl: float) -> float:
+    """cfl_dt (driver.cpp:19-29) from vmax alone."""
+    import ctypes as C
+    from . import _lib
+    g = _lib.mm_grid()
+    g.n[:] = list(grid.n)
+    g.d[:] = list(grid.d)
+    g.radius = grid.radius
+    dt = C.c_double()
+    _lib.check(_lib.lib().mm_cfl_dt(float(vmax), C.byref(g), float(cfl), C.byref(dt)))
+    return dt.value
 
 
 # --------------------------------------------------------------- bench (torchrun)
 def bench_rank(args, rank, world, local):
-    """bench.py --gpus N under torchrun: weak scaling, per-rank 240^3 work
-    (global grid 240 x 240 x (240 N)), cost-weighted z slabs, NCCL halos
-    overlapped with the interior.  `value`: device time of K steps of the
-    overlap schedule (max over ranks); `e2e`: the same K steps with the source
-    sample H2D and the receiver plane D2H (rank 0) every step, wall clock, max
-    over ranks."""
+    """bench.py --gpus N under torchrun, one rank per GPU through the C++ group
+    (NCCL halo planes overlapped with the interior update).
+
+    --scaling weak (default): 240^3 per GPU, global grid 240 x 240 x 240 N;
+    --scaling strong: the global grid fixed at --grid^3 (BASELINE configs[2]
+    512^3, configs[3] 1000^3), cost-weighted legal z cuts.  `value` = global
+    points x K / the max over ranks of the device time of K steps; `e2e`: the
+    same K steps driven step by step through the C ABI with the source sample
+    H2D and the receiver plane D2H (rank 0) every step.  Strong scaling also
+    reports the efficiency of bench.cpp:130-145 against one GPU on the same
+    grid (rank 0 alone, after the group is gone)."""
     import torch
     import torch.distributed as dist
     import paper_2007_06048_b200 as mm
     from . import _lib
     from .driver import SimConfig
+    from .propagator import ZSlabGroup
+    from .scaling import ScalingResult, ScalingRun, compute_efficiency, count_stencil_cost
 
     torch.cuda.set_device(local)
     if not dist.is_initialized():
@@ -402,83 +399,141 @@ def bench_rank(args, rank, world, local):
                 port = sk.getsockname()[1]
             os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK=str(local),
                               MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    edge = args.grid or 240
-    n = (edge, edge, edge * world)
-    cfg = SimConfig(ngrid=n, nsteps=args.warmup, stencil_radius=args.radius)
-    cuts = weighted_cuts(n, cfg.ndamping, args.radius, world)
+        dist.init_process_group("gloo")  # host plumbing; halos go over the group's NCCL
+    strong = getattr(args, "scaling", "weak") == "strong"
+    edge = args.grid or (1000 if strong else 240)
+    n = (edge, edge, edge) if strong else (edge, edge, edge * world)
+    r = args.radius
+    cfg = SimConfig(ngrid=n, nsteps=args.warmup, stencil_radius=r)
+    nd = tuple(cfg.ndamping)
+    cuts = weighted_cuts(n, nd, r, world)
     info = SlabInfo(rank, world, cuts)
-    grid = mm.make_grid(n, cfg.dgrid, args.radius)
-    vp = mm.default_layered_model(grid).vp
-    tr = TorchTransport()
-    # W warm-up steps (engine, receivers, work lists, NCCL communicators)
-    res = run_zslab(mm, cfg, vp, info, tr, device=local, mode=args.mode)
-    eng = res["engine"]
-    rk = ZSlabRank(eng, info, tr, tuple(x // 2 for x in n))
-    w = mm.ricker(cfg.fmax, res["dt"], args.warmup + args.steps).samples[args.warmup:]
-    ext = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
-
-    def timed(e2e: bool):
-        owns = res["owns_receivers"]
-        nrec = n[0] * n[1]
-        host = (torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
-                if e2e and owns else None)
-        if owns:
-            eng.set_receivers(_receivers_local(mm, grid, cfg, info), args.steps)
-        tr.barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        l0 = _lib.kernel_launch_count()
-        t0 = time.perf_counter()
-        e0.record(ext)
-        for s in range(args.steps):
-            rk.step_overlap(float(w[s]))
-            if owns:
-                eng.record(s)
-                if e2e:
-                    eng.copy_trace_step(s, host[s], asynchronous=True)
-        e1.record(ext)
-        eng.synchronize()
-        wall = time.perf_counter() - t0
-        launches = _lib.kernel_launch_count() - l0
-        torch.cuda.synchronize()
-        tr.barrier()
-        return e0.elapsed_time(e1), wall * 1e3, launches, (nrec * 4 if owns else 0)
-
+    grid = mm.make_grid(n, cfg.dgrid, r)
+    vp_loc = layered_slice(n, info.z0, info.nz, r)
+    vmax = 4500.0
+    dt = cfl_dt_vmax(vmax, grid, cfg.cfl)
+    total = args.warmup + args.steps
+    w = mm.ricker(cfg.fmax, dt, total).samples
+    src = tuple(x // 2 for x in n)
+    opts = mm.EngineOptions(ndamping=nd, taper=True)
+    nid = share_nccl_id(rank) if world > 1 else None
+    grp = ZSlabGroup(grid, cuts, rank, None, opts, float(np.float32(dt)), vmax, nccl_id=nid,
+                     device=local, mode=args.mode, vp_local=vp_loc)
+    eng = grp.engine
+    owns = info.z0 <= nd[2] < info.z0 + info.nz
+    nrec = n[0] * n[1]
+    if owns:
+        eng.set_receivers(_receivers_local(mm, grid, cfg, info), total)
+    # warm-up (work lists, NCCL connections, clocks)
+    grp.run(w[:args.warmup], src, record=owns)
+    dist.barrier()
     from .clocks import ClockSampler
     clocks = ClockSampler(local)
     clocks.start()
-    ms, _, launches, _ = timed(False)
+    l0 = _lib.kernel_launch_count()
+    ms = grp.run(w[args.warmup:total], src, record=owns, first_sample=args.warmup)
+    launches = _lib.kernel_launch_count() - l0
     clk = clocks.stop()
-    dev_ms = tr.max(ms)
-    _, wall_ms, _, d2h = timed(True)
-    e2e_ms = tr.max(max(wall_ms, ms))
-    d2h = int(tr.max(float(d2h)))
+    dev_ms = _max(ms)
+    # e2e: step by step through the C ABI, host amplitude in, receiver plane out
+    host = (torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
+            if owns else None)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        grp.step(float(w[args.warmup + s]), src)
+        if owns:
+            eng.record(args.warmup + s)
+            eng.copy_trace_step(args.warmup + s, host[s], asynchronous=True)
+    eng.synchronize()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    e2e_ms = _max(max(wall_ms, ms))
     pts = float(n[0]) * n[1] * n[2]
     value = pts * args.steps / (dev_ms * 1e-3) / 1e9
     e2e = pts * args.steps / (e2e_ms * 1e-3) / 1e9
-    all_launches = int(tr.max(float(launches)) * world) if world > 1 else launches
+    all_launches = int(_max(float(launches)) * world)
+    grp.close()
+    del grp, eng
+    torch.cuda.synchronize()
+    eff = None
+    if strong and world > 1 and getattr(args, "efficiency", True):
+        # one GPU on the same global grid (bench.cpp:130-145 strong, r0 = 1)
+        t1 = None
+        if rank == 0:
+            t1 = _single_gpu_ms_per_step(mm, n, r, nd, dt, w, src, local, args)
+        t1 = _bcast_float(t1)
+        if t1 and t1 > 0:
+            res = ScalingResult("strong", [ScalingRun(1, n, 1, kernel_s=t1 * 1e-3),
+                                           ScalingRun(world, n, 1,
+                                                      kernel_s=dev_ms / args.steps * 1e-3)])
+            compute_efficiency(res)
+            eff = {"efficiency_pct": round(res.runs[1].efficiency_pct, 2),
+                   "one_gpu_ms_per_step": round(t1, 4),
+                   "definition": "t1 * 1 / (tN * N), bench.cpp:130-145 strong"}
     if rank == 0:
-        print(json.dumps({
+        cost = count_stencil_cost("acoustic_iso_cd", r)
+        line = {
             "metric": "Gpoints/s (grid-point updates/sec) acoustic_iso_cd 8th-order",
             "value": round(value, 3), "unit": "Gpoints/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (default two-layer vp model 1500/4500, Ricker source)",
-            "config": {"workload": f"acoustic_iso_cd r={args.radius} {n[0]}x{n[1]}x{n[2]} grid, "
-                                   f"z-slabs {cuts}, NCCL halo exchange overlapped "
-                                   "with the interior (weak scaling: 240^3 per GPU)",
-                       "grid": list(n), "cuts": cuts, "radius": args.radius,
-                       "balance": round(balance(n, cfg.ndamping, cuts), 4), "mode": args.mode,
-                       "l2": "working set > 126 MB L2 per GPU; no flush"},
+            "config": {"workload": (f"acoustic_iso_cd r={r} {n[0]}x{n[1]}x{n[2]} grid, "
+                                    f"{world} z-slabs {cuts}, NCCL halo planes overlapped "
+                                    "with the interior (C++ group, mm_cd_group_run)"
+                                    + ("" if strong else "; weak scaling: 240^3 per GPU")),
+                       "grid": list(n), "cuts": cuts, "radius": r,
+                       "balance": round(balance(n, nd, cuts), 4), "mode": args.mode,
+                       "l2": "working set > 126 MB L2 per GPU; no flush",
+                       "flops_per_point": cost.flops_per_point,
+                       "arithmetic_intensity": round(cost.arithmetic_intensity, 4)},
             "e2e": {"value": round(e2e, 3), "unit": "Gpoints/s", "h2d_bytes_per_step": 4 * world,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": 4 * nrec},
             "gpu_launches": all_launches,
             "clocks": clk,
-        }), flush=True)
+        }
+        if eff:
+            line["parallel_efficiency"] = eff
+        print(json.dumps(line), flush=True)
+    dist.barrier()
     dist.destroy_process_group()
     return 0
+
+
+def _max(v: float) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _bcast_float(v):
+    import torch.distributed as dist
+    obj = [v]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def _single_gpu_ms_per_step(mm, n, r, nd, dt, w, src, device, args):
+    """ms/step of one engine on the whole grid (the strong-scaling baseline),
+    or None when the grid does not fit the GPU."""
+    import torch
+    free, _ = torch.cuda.mem_get_info(device)
+    pts = (n[0] + 2 * r + 32) * (n[1] + 2 * r) * (n[2] + 2 * r)
+    if 6.5 * 4 * pts > 0.9 * free:
+        return None
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0), r)
+    vp = layered_slice(n, 0, n[2], r)
+    e = mm.AcousticCdEngine(grid, (0, 0, 0), n, vp, mm.EngineOptions(ndamping=nd, taper=True),
+                            float(np.float32(dt)), 4500.0, device=device, mode=args.mode)
+    k = max(3, min(args.steps, 50))
+    e.run(w[:3], src, record=False)
+    ms = e.run(w[:k], src, record=False)
+    e.close()
+    return ms / k
 
 
 def _receivers_local(mm, grid, cfg, info):

@@ -87,11 +87,28 @@ class AcousticCdEngine:
         self._nrec = 0
         self._cap = 0
 
+    @classmethod
+    def _view(cls, handle, grid: Grid3D, offset, global_n, opts, device, mode):
+        """A non-owning wrapper of an engine another object owns (the slab
+        engine of a ZSlabGroup)."""
+        self = cls.__new__(cls)
+        self._h = handle
+        self._grid = grid
+        self.offset = tuple(int(x) for x in offset)
+        self.global_n = tuple(int(x) for x in global_n)
+        self.mode = mode
+        self.device = device
+        self.options = opts
+        self._nrec = 0
+        self._cap = 0
+        self._owned = False
+        return self
+
     # -- lifetime ---------------------------------------------------------
     def close(self):
-        if self._h:
+        if self._h and getattr(self, "_owned", True):
             lib().mm_cd_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -274,6 +291,90 @@ class AcousticCdEngine:
         fn = lib().mm_cd_next_halo_planes if next_field else lib().mm_cd_halo_planes
         check(fn(self._h, int(side), int(which), C.byref(p), C.byref(n)))
         return p.value, n.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (mm_nccl_get_unique_id), made by rank 0 and
+    shared with the other ranks by the host runtime."""
+    buf = (C.c_ubyte * 128)()
+    check(lib().mm_nccl_get_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def validate_cuts_native(cuts, nz: int, nd_z: int, radius: int) -> None:
+    """mm_zslab_validate_cuts (ref: dist.cpp:119-132)."""
+    arr = (C.c_int * len(cuts))(*cuts)
+    check(lib().mm_zslab_validate_cuts(arr, len(cuts) - 1, int(nz), int(nd_z), int(radius)))
+
+
+class ZSlabGroup:
+    """One rank of the multi-GPU z-slab run (mm_cd_group_*, group.cu): its slab
+    engine and NCCL halo exchange, driven from C++.
+
+    ref: run_distributed_rank (dist.cpp:144-267) with dims {1, 1, P}."""
+
+    def __init__(self, grid: Grid3D, cuts, rank: int, vp_global: Optional[np.ndarray],
+                 opts: Optional[EngineOptions], dt: float, vmax: float, *,
+                 nccl_id: Optional[bytes] = None, device: int = 0, mode: str = "fast",
+                 vp_local: Optional[np.ndarray] = None):
+        opts = opts or EngineOptions()
+        world = len(cuts) - 1
+        r = grid.radius
+        z0, z1 = int(cuts[rank]), int(cuts[rank + 1])
+        # the rank's ghosted slice of the ghosted global model (dist.cpp:171-180)
+        if vp_local is None:
+            vp_local = vp_global[:, :, z0:z1 + 2 * r]
+        vp_loc = np.ascontiguousarray(vp_local, dtype=np.float32)
+        if vp_loc.shape != (grid.shape[0], grid.shape[1], z1 - z0 + 2 * r):
+            raise ValueError("vp_local must be the rank's ghosted slab")
+        g = _lib.mm_grid()
+        g.n[:] = list(grid.n)
+        g.d[:] = list(grid.d)
+        g.radius = r
+        arr = (C.c_int * len(cuts))(*[int(c) for c in cuts])
+        idb = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes")
+            idb = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+        h = C.c_void_p()
+        self._h = None
+        check(lib().mm_cd_group_create(C.byref(g), arr, world, int(rank),
+                                       C.cast(idb, C.c_void_p) if idb is not None else None,
+                                       _fptr(vp_loc), C.byref(opts.to_c()), C.c_float(dt),
+                                       float(vmax), int(device), _MODES[mode], C.byref(h)))
+        self._h = h
+        self.rank, self.world, self.cuts = rank, world, list(cuts)
+        self.z0, self.nz = z0, z1 - z0
+        eh = C.c_void_p()
+        check(lib().mm_cd_group_engine(self._h, C.byref(eh)))
+        lgrid = Grid3D((grid.n[0], grid.n[1], self.nz), grid.d, r)
+        self.engine = AcousticCdEngine._view(eh, lgrid, (0, 0, z0), grid.n, opts, device, mode)
+
+    def close(self):
+        if self._h:
+            self.engine._h = None
+            lib().mm_cd_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, amp: float, src_global: Optional[Sequence[int]] = None):
+        check(lib().mm_cd_group_step(self._h, C.c_float(amp),
+                                     _i3(*src_global) if src_global is not None else None))
+
+    def run(self, amps: np.ndarray, src_global: Optional[Sequence[int]] = None,
+            record: bool = True, first_sample: int = 0) -> float:
+        amps = np.ascontiguousarray(amps, dtype=np.float32)
+        ms = C.c_float()
+        check(lib().mm_cd_group_run(self._h, _fptr(amps), amps.size,
+                                    _i3(*src_global) if src_global is not None else None,
+                                    int(record), int(first_sample), C.byref(ms)))
+        return ms.value
 
 
 class AcousticVdEngine:

@@ -139,3 +139,59 @@ def test_gloo_world2_zslab_equals_single_rank():
         assert np.array_equal(field[4:-4, 4:-4], full[4:-4, 4:-4, z0:z0 + nz]), rank
         covered += nz
     assert covered == n[2]
+
+
+# ------------------------------------------------------------ group host plumbing
+def test_layered_slice_equals_global_model_slices(mm):
+    """Each rank builds its ghosted slab of default_layered_model without the
+    global volume (dist.cpp:171-180 slices the global one): identical."""
+    from paper_2007_06048_b200 import dist as D
+    n = (20, 22, 41)
+    full = mm.default_layered_model(mm.make_grid(n, (20.0, 20.0, 20.0))).vp
+    for cuts in ([0, 41], [0, 15, 41], [0, 12, 20, 29, 41]):
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            assert np.array_equal(D.layered_slice(n, a, b - a, 4), D.local_vp(full, 4, a, b - a))
+
+
+def test_native_cut_validation_matches_reference_rule(mm):
+    """mm_zslab_validate_cuts (C ABI) == dist.cpp:119-132 == validate_cuts."""
+    from paper_2007_06048_b200 import dist as D
+    from paper_2007_06048_b200.propagator import validate_cuts_native
+    validate_cuts_native([0, 31, 64], 64, 27, 4)
+    for bad in ([0, 30, 64], [0, 34, 64], [0, 40, 42, 64]):
+        with pytest.raises(mm.ConfigError):
+            validate_cuts_native(bad, 64, 27, 4)
+        with pytest.raises(mm.ConfigError):
+            D.validate_cuts(bad, 64, 27, 4)
+    for p in (2, 4, 8):
+        validate_cuts_native(D.weighted_cuts((1000, 1000, 1000), (27, 27, 27), 4, p),
+                             1000, 27, 4)
+
+
+def _id_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2007_06048_b200 import dist as D
+        q.put((rank, D.share_nccl_id(rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_nccl_id_broadcast():
+    """Every rank of the C++ group gets rank 0's 128-byte NCCL id through the
+    torch.distributed plumbing (bench_rank / run_zslab)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(got[0]) == 128 and got[0] == got[1]
