@@ -151,7 +151,7 @@ def ncu_traffic(workload, kernel):
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_reference_run(n, nsteps, nthreads, propagator="acoustic_iso_cd"):
+def cpu_reference_run(n, nsteps, nthreads, propagator="acoustic_iso_cd", want_traces=False):
     from oracle.oracle import Oracle, available, nproc
     kind = "reference" if available("reference") else "port"
     o = Oracle(kind)
@@ -171,7 +171,25 @@ def cpu_reference_run(n, nsteps, nthreads, propagator="acoustic_iso_cd"):
         out = o.run(n, vp, nsteps=nsteps)
         threads = 1
     gpts = n[0] * n[1] * n[2] * nsteps / out["kernel_seconds"] / 1e9
+    if want_traces:
+        return gpts, kind, threads, out["kernel_seconds"], out["traces"]
     return gpts, kind, threads, out["kernel_seconds"]
+
+
+def trace_parity(mm, n, nsteps, ref_traces, mode):
+    """The GPU engine's run() (the device loop, mm_run) on the CPU baseline's
+    own workload and steps against the reference's trace matrix: rel L2,
+    max-abs and bit equality (north_star: rel L2 <= 1e-5, max-abs reported)."""
+    cfg = mm.SimConfig(ngrid=n, nsteps=nsteps)
+    model = mm.default_layered_model(mm.make_grid(n, cfg.dgrid))
+    rec, _ = mm.run(cfg, model, mode=mode)
+    got = rec.traces.astype(np.float64)
+    want = ref_traces.astype(np.float64)
+    diff = np.abs(got - want)
+    return {"rel_l2": float(np.linalg.norm(diff) / max(np.linalg.norm(want), 1e-300)),
+            "max_abs": float(diff.max()), "steps": nsteps, "receivers": int(want.shape[0]),
+            "bitwise": bool(np.array_equal(rec.traces, ref_traces)),
+            "vs": "the reference's run() traces (oracle/_ref, full receiver matrix)"}
 
 
 def cpu_sample_steps(n, requested):
@@ -313,7 +331,11 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (default two-layer vp model 1500/4500, Ricker source)",
         "config": {"workload": f"acoustic_iso_cd r={r} {edge}^3 grid, nd=27 CPML, taper, "
-                               f"{nrec} surface receivers (BASELINE configs[1])",
+                               f"{nrec} surface receivers"
+                               + (" (BASELINE configs[1])" if edge == 240 and r == 4 else
+                                  " (BASELINE configs[2])" if edge == 512 and r == 4 else
+                                  " (BASELINE configs[3] at N = 1)" if edge == 1000 else
+                                  " (BASELINE configs[4] radius sweep)" if edge == 512 else ""),
                    "grid": list(n), "radius": r, "ndamping": list(nd), "mode": args.mode,
                    "cpml_path": eng.cpml_path(),
                    "flops_per_point": cost.flops_per_point,
@@ -338,11 +360,12 @@ def run_ours(args):
         ns = cpu_sample_steps(n, args.cpu_sample_steps)
         from oracle.oracle import nproc
         cores = nproc()
-        gpts, kind, threads, secs = cpu_reference_run(n, ns, cores)
+        gpts, kind, threads, secs, ref_tr = cpu_reference_run(n, ns, cores, want_traces=True)
         line["cpu_baseline"] = {"value": round(gpts, 5), "unit": UNIT, "cores": threads,
                                 "kind": kind,
                                 "sample": f"{edge}^3 x {ns} steps from t=0 ({secs:.1f} s), "
                                           "run() Target::Parallel"}
+        line["parity"] = trace_parity(mm, n, ns, ref_tr, args.mode)
     print(json.dumps(line), flush=True)
     return 0
 

@@ -15,9 +15,10 @@
 //    of a circular stage buffer.  The run arrays are the reference's per-slab
 //    zero-halo boxes, so TMA's out-of-bounds zero fill IS the reference's zero
 //    halo (cpml.hpp:77-99).
-//  * point-wise streams (p_prev, c, zeta_x/y/z, dpsi_z from k_p1) have no
-//    reuse: consumers read them with 16-byte loads straight into registers,
-//    issued before the plane's shared-memory work so their latency overlaps it.
+//  * the point-wise streams (p_prev, c, zeta_x/y/z, dpsi_z from k_p1) have no
+//    reuse; lane 1 stages them by TMA too, per plane, in the same circular
+//    stage buffer as the psi boxes (16-byte LDG into registers left the
+//    lockstep consumers waiting on the loads: 12 % slower).
 //  * new p and zeta go out with 16-byte stores.
 #pragma once
 

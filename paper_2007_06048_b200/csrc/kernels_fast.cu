@@ -414,7 +414,7 @@ public:
         if (ov && inner_late_ == 1) fork_inner();  // (issue order only: still from the start)
         const int t2 = timer.begin("boundary", s);
         if (fc)
-            launch_boundary(p, 0, lay_.n[2], s);
+            launch_boundary(p, 0, lay_.n[2], s, t2 < 0);  // (timer events break the PDL pair)
         else
             strict_update(p, 2, 0, lay_.n[2], s);
         timer.end(t2, s);
@@ -714,10 +714,17 @@ private:
             return ensure_dpz(p);
     }
 
-    void launch_boundary(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) {
-        launch_boundary(p, ZRanges{{z_lo, z_hi}}, s);
+    // after_p1: k_p1 is the kernel right before on `s` (the step): k_bnd may
+    // then launch programmatically (PDL) -- its p_cur ring streams before
+    // griddepcontrol.wait, which is safe only behind a kernel that does not
+    // write p_cur.  Any other predecessor (the epilogue, an injection, the
+    // interior kernel of the plane-range schedule) gets a plain launch.
+    void launch_boundary(const StepParams& p, int z_lo, int z_hi, cudaStream_t s,
+                         bool after_p1 = false) {
+        launch_boundary(p, ZRanges{{z_lo, z_hi}}, s, after_p1);
     }
-    void launch_boundary(const StepParams& p, const ZRanges& zr, cudaStream_t s) {
+    void launch_boundary(const StepParams& p, const ZRanges& zr, cudaStream_t s,
+                         bool after_p1 = false) {
         if constexpr (kBnd && kP1) {
             Work& w = bnd_work(p, zr);
             if (w.empty) return;
@@ -753,10 +760,11 @@ private:
             bp_.wq = WorkQueue{w.ctr.ptr, w.nitems};
             // tuning "bnd_ctas" (diagnostics): cap the CTA count (more items per CTA)
             const int ctas = std::min(w.ctas, bnd_cap_);
+            const bool pdl = pdl_ && after_p1;
             if (order_ == 2)
-                launch_pdl(k_bnd<R, 2>, ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
+                launch_pdl(k_bnd<R, 2>, ctas, BC::NT, BC::SMEM, s, pdl, maps_, bp_);
             else
-                launch_pdl(k_bnd<R, 1>, ctas, BC::NT, BC::SMEM, s, pdl_, maps_, bp_);
+                launch_pdl(k_bnd<R, 1>, ctas, BC::NT, BC::SMEM, s, pdl, maps_, bp_);
             note_launches(1);
             MM_CUDA(cudaGetLastError());
         }
