@@ -410,38 +410,46 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                     xs[4 * h + 2] = v.z;
                     xs[4 * h + 3] = v.w;
                 }
-                float two_p0[4];
+                // lane pairs (FADD2, fast_common.cuh): pair h = points 2h, 2h + 1
+                auto px = [&](const float* v, int h, int m) {
+                    return f2(v[C::HX + 2 * h + m], v[C::HX + 2 * h + 1 + m]);
+                };
+                F2 two_p0[2], d2x[2], d2y[2], d2z[2];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) two_p0[e] = 2.0f * xs[C::HX + e];
+                for (int h = 0; h < 2; ++h) {
+                    const F2 c = px(xs, h, 0);
+                    two_p0[h] = fa2<ORD>(c, c);  // T(2) * c (exact)
+                    d2x[h] = d2y[h] = d2z[h] = f2zero();
+                }
                 // second derivatives, one axis at a time (stencil.hpp:86-91)
-                float d2x[4] = {0.f, 0.f, 0.f, 0.f}, d2y[4] = {0.f, 0.f, 0.f, 0.f},
-                      d2z[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        d2x[e] = d2_term<ORD>(d2x[e], P.c2[0][m - 1], xs[C::HX + e + m],
-                                              xs[C::HX + e - m], two_p0[e]);
+                    for (int h = 0; h < 2; ++h)
+                        d2x[h] = d2_term2<ORD>(d2x[h], P.c2[0][m - 1], px(xs, h, m), px(xs, h, -m),
+                                               two_p0[h]);
 #pragma unroll
                 for (int m = 1; m <= R; ++m) {
-                    const float4 u = lds4(S + m * C::BX), d = lds4(S - m * C::BX);
+                    F2 u[2], d[2];
+                    lds4x2(S + m * C::BX, u[0], u[1]);
+                    lds4x2(S - m * C::BX, d[0], d[1]);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        d2y[e] = d2_term<ORD>(d2y[e], P.c2[1][m - 1], comp(u, e), comp(d, e),
-                                              two_p0[e]);
+                    for (int h = 0; h < 2; ++h)
+                        d2y[h] = d2_term2<ORD>(d2y[h], P.c2[1][m - 1], u[h], d[h], two_p0[h]);
                 }
 #pragma unroll
                 for (int m = 1; m <= R; ++m) {
-                    const float4 u = lds4(ring + wo[R + m]);
-                    const float4 d = lds4(ring + wo[R - m]);
+                    F2 u[2], d[2];
+                    lds4x2(ring + wo[R + m], u[0], u[1]);
+                    lds4x2(ring + wo[R - m], d[0], d[1]);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        d2z[e] = d2_term<ORD>(d2z[e], P.c2[2][m - 1], comp(u, e), comp(d, e),
-                                              two_p0[e]);
+                    for (int h = 0; h < 2; ++h)
+                        d2z[h] = d2_term2<ORD>(d2z[h], P.c2[2][m - 1], u[h], d[h], two_p0[h]);
                 }
                 // dpsi_x, dpsi_y from the psi boxes (central_derivative_at)
-                float dpx[4] = {0.f, 0.f, 0.f, 0.f}, dpy[4] = {0.f, 0.f, 0.f, 0.f};
-                float4 pp, cv, zx = make_float4(0.f, 0.f, 0.f, 0.f), zy = zx, zz = zx, dz = zx;
+                F2 dpx[2] = {f2zero(), f2zero()}, dpy[2] = {f2zero(), f2zero()};
+                F2 pp[2], cv[2], zx[2] = {f2zero(), f2zero()}, zy[2] = {f2zero(), f2zero()},
+                                 zz[2] = {f2zero(), f2zero()}, dz[2] = {f2zero(), f2zero()};
                 {
                     const int st = nq % C::NQD;
                     const int qsz = T.qsize + (zr >= 0 ? C::TILE : 0) + (zex >= 0 ? C::TILE : 0);
@@ -449,13 +457,13 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                     const float* Q = qring + qo;
                     mbar_wait(fullQ + 8 * st, (nq / C::NQD) & 1);
                     qo += qsz;
-                    pp = lds4(Q + toff);
-                    cv = lds4(Q + C::TILE + toff);
-                    if (fx) zx = lds4(Q + T.o_zx + toff);
-                    if (y_in_zy) zy = lds4(Q + (zyside == 0 ? T.o_zy0 : T.o_zy1) + toff);
-                    if (zr >= 0) zz = lds4(Q + T.qsize + toff);
+                    lds4x2(Q + toff, pp[0], pp[1]);
+                    lds4x2(Q + C::TILE + toff, cv[0], cv[1]);
+                    if (fx) lds4x2(Q + T.o_zx + toff, zx[0], zx[1]);
+                    if (y_in_zy) lds4x2(Q + (zyside == 0 ? T.o_zy0 : T.o_zy1) + toff, zy[0], zy[1]);
+                    if (zr >= 0) lds4x2(Q + T.qsize + toff, zz[0], zz[1]);
                     // dpsi_z (k_p1); +0 where no psi_z reaches the window
-                    if (zex >= 0) dz = lds4(Q + T.qsize + (zr >= 0 ? C::TILE : 0) + toff);
+                    if (zex >= 0) lds4x2(Q + T.qsize + (zr >= 0 ? C::TILE : 0) + toff, dz[0], dz[1]);
                     if (fx) {
                         float ps[4 + 2 * C::HX];
 #pragma unroll
@@ -469,9 +477,9 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
 #pragma unroll
                         for (int m = 1; m <= R; ++m)
 #pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                dpx[e] = acc<ORD>(dpx[e], P.c1[0][m - 1],
-                                                  fs<ORD>(ps[C::HX + e + m], ps[C::HX + e - m]));
+                            for (int h = 0; h < 2; ++h)
+                                dpx[h] = acc2<ORD>(dpx[h], P.c1[0][m - 1],
+                                                   fs2<ORD>(px(ps, h, m), px(ps, h, -m)));
                     }
                     if (fy0 || fy1) {
                         const float* q0 = Q + T.o_psy0 + psy_off;
@@ -489,10 +497,11 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                                 up.x += a.x, up.y += a.y, up.z += a.z, up.w += a.w;
                                 dn.x += b.x, dn.y += b.y, dn.z += b.z, dn.w += b.w;
                             }
+                            const F2 u[2] = {f2(up.x, up.y), f2(up.z, up.w)};
+                            const F2 d[2] = {f2(dn.x, dn.y), f2(dn.z, dn.w)};
 #pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                dpy[e] = acc<ORD>(dpy[e], P.c1[1][m - 1],
-                                                  fs<ORD>(comp(up, e), comp(dn, e)));
+                            for (int h = 0; h < 2; ++h)
+                                dpy[h] = acc2<ORD>(dpy[h], P.c1[1][m - 1], fs2<ORD>(u[h], d[h]));
                         }
                     }
                     __syncwarp();
@@ -506,44 +515,56 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
 
                 // reference: drive = d2p*ik + dpsi; zeta = b*zeta + a*drive;
                 // term = drive + zeta; lap = (term_x + term_y) + term_z
-                float out[4], drx[4], dry[4], drz[4];
-                float nzx[4] = {0.f, 0.f, 0.f, 0.f}, nzy[4] = {0.f, 0.f, 0.f, 0.f},
-                      nzz[4] = {0.f, 0.f, 0.f, 0.f};
+                F2 drx[2], dry[2], drz[2];
+                F2 nzx[2] = {f2zero(), f2zero()}, nzy[2] = {f2zero(), f2zero()},
+                   nzz[2] = {f2zero(), f2zero()};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    drx[e] = acc<ORD>(dpx[e], d2x[e], axk[e]);
-                    dry[e] = acc<ORD>(dpy[e], d2y[e], ayk);
-                    drz[e] = acc<ORD>(comp(dz, e), d2z[e], azk);
+                for (int h = 0; h < 2; ++h) {
+                    drx[h] = fa2<ORD>(fm2v<ORD>(axk[2 * h], axk[2 * h + 1], d2x[h]), dpx[h]);
+                    dry[h] = fa2<ORD>(fm2<ORD>(ayk, d2y[h]), dpy[h]);
+                    drz[h] = fa2<ORD>(fm2<ORD>(azk, d2z[h]), dz[h]);
                 }
                 // zeta updates only where a run holds the row / plane (uniform
                 // branches: no FP spent on the other tiles' terms)
                 if (fx) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        nzx[e] = acc<ORD>(fm<ORD>(axa[e], drx[e]), axb[e], comp(zx, e));
+                    for (int h = 0; h < 2; ++h)
+                        nzx[h] = fa2<ORD>(fm2v<ORD>(axa[2 * h], axa[2 * h + 1], drx[h]),
+                                          fm2v<ORD>(axb[2 * h], axb[2 * h + 1], zx[h]));
                 }
                 if (y_in_zy) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        nzy[e] = acc<ORD>(fm<ORD>(aya, dry[e]), ayb, comp(zy, e));
+                    for (int h = 0; h < 2; ++h)
+                        nzy[h] = fa2<ORD>(fm2<ORD>(aya, dry[h]), fm2<ORD>(ayb, zy[h]));
                 }
                 if (zr >= 0) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        nzz[e] = acc<ORD>(fm<ORD>(aza, drz[e]), azb, comp(zz, e));
+                    for (int h = 0; h < 2; ++h)
+                        nzz[h] = fa2<ORD>(fm2<ORD>(aza, drz[h]), fm2<ORD>(azb, zz[h]));
                 }
+                float out[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float lap = fa<ORD>(fa<ORD>(fa<ORD>(drx[e], nzx[e]), fa<ORD>(dry[e], nzy[e])),
-                                              fa<ORD>(drz[e], nzz[e]));
-                    out[e] = acc<ORD>(fs<ORD>(two_p0[e], comp(pp, e)), comp(cv, e), lap);
+                for (int h = 0; h < 2; ++h) {
+                    const F2 lap = fa2<ORD>(fa2<ORD>(fa2<ORD>(drx[h], nzx[h]), fa2<ORD>(dry[h], nzy[h])),
+                                            fa2<ORD>(drz[h], nzz[h]));
+                    float c0, c1;
+                    unf2(cv[h], c0, c1);
+                    unf2(fa2<ORD>(fs2<ORD>(two_p0[h], pp[h]), fm2v<ORD>(c0, c1, lap)), out[2 * h],
+                         out[2 * h + 1]);
                 }
+                float vzx[4], vzy[4], vzz[4];
+                unf2(nzx[0], vzx[0], vzx[1]);
+                unf2(nzx[1], vzx[2], vzx[3]);
+                unf2(nzy[0], vzy[0], vzy[1]);
+                unf2(nzy[1], vzy[2], vzy[3]);
+                unf2(nzz[0], vzz[0], vzz[1]);
+                unf2(nzz[1], vzz[2], vzz[3]);
                 // stores: p_next inside the box, zeta where a run holds the point
                 if (pany) {
                     st4(pn_p + fo, out, pok, pall);
-                    if (fx) st4(zx_p + o * zx_step, nzx, pok, pall);
-                    if (y_in_zy) st4(zy_p + o * zy_step, nzy, pok, pall);
-                    if (zr >= 0) st4(zz_p, nzz, pok, pall);
+                    if (fx) st4(zx_p + o * zx_step, vzx, pok, pall);
+                    if (y_in_zy) st4(zy_p + o * zy_step, vzy, pok, pall);
+                    if (zr >= 0) st4(zz_p, vzz, pok, pall);
                 }
             } else {
                 mbar_wait(fullP + 8 * s, ph);
