@@ -139,13 +139,16 @@ def measured_peak():
 
 def ncu_traffic(workload, kernel):
     """dram read+write bytes per launch of `kernel` from the committed ncu
-    summary (profiles/ncu_summary.json, one `ncu --set full` capture)."""
+    summary (profiles/ncu_summary.json, `ncu --set full` captures by
+    tools/refresh_profiles.sh); "pass1" sums its x/y and z launches."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
-        d = json.loads(p.read_text())
-        return d.get(workload, {}).get(kernel, {}).get("dram_bytes_per_launch")
+        d = json.loads(p.read_text()).get(workload, {})
+        if kernel == "pass1" and "pass1_z" in d:
+            return sum(d[k]["dram_bytes_per_launch"] for k in ("pass1_z", "pass1_xy") if k in d)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -317,7 +320,7 @@ def run_ours(args):
     achieved = kb[dominant] / (kms[dominant] * 1e-3) / 1e9
     step_bytes, _, _ = byte_model(n, nd)
     step_gbs = step_bytes * args.steps / (ms * 1e-3) / 1e9
-    traffic = ncu_traffic(f"{edge}^3", dominant)
+    traffic = ncu_traffic(f"{edge}^3" + ("" if r == 4 else f" r{r}"), dominant)
     per_kernel = {k: {"ms": round(kms[k], 4), "launches": klaunch[k],
                       "algorithmic_bytes": kb.get(k),
                       "achieved_gbs": (round(kb[k] / (kms[k] * 1e-3) / 1e9, 1)

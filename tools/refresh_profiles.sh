@@ -40,4 +40,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:k_c
     -o $O/full_cpml_240 -f $P --grid 240 --variants "cpml_fused=1" > $O/ncu_cpml.log 2>&1
 echo "ncu cpml rc=$?"
 for f in $O/*.ncu-rep; do ncu -i $f --page raw --csv > ${f%.ncu-rep}_raw.csv 2>/dev/null; done
+# gpurun brings back at most 64 MiB: keep the raw exports, drop the large reports
+find $O -name '*.ncu-rep' -size +12M -delete
+du -sh $O
 echo done
