@@ -49,6 +49,7 @@ const Tunable kTunables[] = {
     {"debug_sync", 0},   // (diagnostics) synchronize after every kernel (1) or every step (2)
     {"l2_promo", 2},     // TMA L2 promotion: 0 none, 1 64 B, 2 128 B, 3 256 B
     {"inner_zt", 48},    // k_inner planes per work item (target)
+    {"inner_ctas", 0},   // cap on the interior kernel's CTAs beside the CPML kernels (0: every slot)
     {"bnd_zt", 12},      // k_bnd planes per work item (target)
     {"p1_zt", 16},       // k_p1 planes per work item (target)
     {"zslabs", -1},      // Z slabs: -1 auto, 0 k_bnd tiles, 1 k_zslab after k_inner, 2 k_zslab columns

@@ -276,6 +276,7 @@ public:
         MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inner<R, 2>, IC::NT,
                                                               IC::SMEM));
         inner_per_sm_ = std::max(1, per_sm);
+        inner_cap_ = tuning("inner_ctas") > 0 ? (int)tuning("inner_ctas") : 1 << 30;
         if constexpr (kBnd) {
             MM_CUDA(cudaFuncSetAttribute(k_bnd<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)BC::SMEM));
@@ -647,9 +648,9 @@ private:
                     k_zslab<R, 1><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
             }
         } else if (order_ == 2) {
-            k_inner<R, 2><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
+            k_inner<R, 2><<<std::min(w.ctas, inner_cap_), IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
         } else {
-            k_inner<R, 1><<<w.ctas, IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
+            k_inner<R, 1><<<std::min(w.ctas, inner_cap_), IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
         }
         note_launches(1);
         MM_CUDA(cudaGetLastError());
@@ -1113,6 +1114,7 @@ private:
     int device_;
     int order_ = 2;
     int sms_ = 148, inner_per_sm_ = 1, bnd_per_sm_ = 1, cpml_per_sm_ = 1;
+    int inner_cap_ = 1 << 30;
     bool cpml_on_ = false, dbg_ = false;
     int cpml_zt_ = 0, inner_late_ = 0, bnd_kinds_ = 7, bnd_cap_ = 1 << 30, p1_axes_ = 7;
     CUtensorMap cm_pc_[3], cm_tile_[3], cm_cv_;

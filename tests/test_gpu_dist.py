@@ -51,8 +51,8 @@ def _layered(mm, n, r=4):
     return grid, mm.default_layered_model(grid)
 
 
-@pytest.mark.parametrize("fs", [False, True])
-def test_group_world1_equals_single_engine(mm, fs):
+@pytest.mark.parametrize("fs,with_comm", [(False, False), (True, True)])
+def test_group_world1_equals_single_engine(mm, fs, with_comm):
     """The C++ group with one rank (no halo partner) runs the group schedule
     (pass 1, edge-free interior with the interior kernel on its side stream,
     epilogue with the slab-centre check) and equals one engine bitwise --
@@ -68,7 +68,11 @@ def test_group_world1_equals_single_engine(mm, fs):
     one = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax)
     one.set_receivers(geo.receivers, steps)
     one.run(w, src, record=True)
-    g = ZSlabGroup(grid, [0, n[2]], 0, model.vp, opts, dt, model.vmax)
+    nid = None
+    if with_comm:  # a one-rank NCCL communicator (ncclCommInitRank / CommDestroy)
+        from paper_2007_06048_b200.propagator import nccl_unique_id
+        nid = nccl_unique_id()
+    g = ZSlabGroup(grid, [0, n[2]], 0, model.vp, opts, dt, model.vmax, nccl_id=nid)
     g.engine.set_receivers(geo.receivers, steps)
     g.run(w[:25], src, record=True)
     for s in range(25, steps):                # host-driven steps continue the run
