@@ -246,22 +246,33 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, InnerCfg<R>::MINB)
 // k_zslab streams whole z columns of the inner x-y box: planes inside
 // [zi_lo, zi_hi) get the plain update, the Z-slab planes outside it the pass-2
 // formula along z (update_damping_pass2, propagator_impl.hpp:125-152; dpsi_x,
-// dpsi_y, zeta_x, zeta_y are masked to 0 there).  Same 64 x 16 tiles and TMA
-// pipeline as k_inner.  The z window is read from a ring of
-// NS = 2R+1+lead shared slots (no register queue, so the loop is not unrolled
-// and the code stays small), dpsi_z (k_p1) and zeta_z come straight from
-// global memory.
+// dpsi_y, zeta_x, zeta_y are masked to 0 there).  It serves the inner box at
+// r > 4 (k_inner's register queue would unroll the z loop 2R+1 = 17 deep and
+// overflow the instruction cache) and, optionally, the Z slabs at r <= 4.
+// Same 64 x 16 tiles as k_inner; the z window is read from a ring of
+// NS = 2R+1+lead shared slots through a per-thread array of slot offsets
+// rotated once per plane (no register queue, no unrolled loop, no modular
+// slot arithmetic).  8 consumer warps + 1 producer warp: lane 0 pulls work
+// items (4-slot item ring) and streams the p_cur ring, lane 1 the p_prev / c
+// stages, each gated by its own empty barriers, so the consumers never issue
+// TMA and the ring runs as far ahead as its depth allows.  dpsi_z (k_p1) and
+// zeta_z come from global memory one plane ahead.  Arithmetic on lane pairs
+// (FADD2), reference order (bit-exact for ORD 2).
 template <int R>
 struct ZSlabCfg {
     using I = InnerCfg<R>;
     static constexpr int NS = 2 * R + 1 + (R <= 4 ? 3 : 2);
-    static constexpr int NQ = R <= 4 ? 4 : 2;
-    static constexpr size_t SMEM =
-        sizeof(float) * (size_t)(NS * I::PLANE + NQ * 2 * I::TILE) + 8 * (NS + NQ) + 16;
+    static constexpr int NQ = R <= 4 ? 4 : 3;
+    static constexpr int NC = I::NT;       // consumer threads
+    static constexpr int NT = NC + 32;     // + producer warp
+    static constexpr int NI = 4;           // work-item slots
+    static constexpr int NBAR = 2 * NS + 2 * NQ + 4 * NI;
+    static constexpr size_t SMEM = sizeof(float) * (size_t)(NS * I::PLANE + NQ * 2 * I::TILE) +
+                                   8 * NBAR + 16 * NI + 64;
 };
 
 template <int R, int ORD>
-__global__ void __launch_bounds__(InnerCfg<R>::NT, 1)
+__global__ void __launch_bounds__(ZSlabCfg<R>::NT, 1)
     k_zslab(const __grid_constant__ CUtensorMap tm_pc, const __grid_constant__ CUtensorMap tm_pp,
             const __grid_constant__ CUtensorMap tm_cv, const InnerParams P) {
     using C = InnerCfg<R>;
@@ -270,57 +281,101 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
     float* qring = ring + Z::NS * C::PLANE;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(qring + Z::NQ * 2 * C::TILE);
-    const uint32_t barP = smem_u32(bars), barQ = smem_u32(bars + Z::NS);
+    int4* items = reinterpret_cast<int4*>(qring + Z::NQ * 2 * C::TILE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(items + Z::NI);
+    const uint32_t fullP = smem_u32(bars), emptyP = fullP + 8 * Z::NS;
+    const uint32_t fullQ = emptyP + 8 * Z::NS, emptyQ = fullQ + 8 * Z::NQ;
+    const uint32_t fullI = emptyQ + 8 * Z::NQ, emptyI = fullI + 8 * Z::NI;
+    const uint32_t fullS = emptyI + 8 * Z::NI, emptyS = fullS + 8 * Z::NI;
     const int tid = threadIdx.x;
-    const int tx = tid % C::TXT, ty = tid / C::TXT;
     const Layout L = P.lay;
 
     if (tid == 0) {
         prefetch_tmap(&tm_pc);
         prefetch_tmap(&tm_pp);
         prefetch_tmap(&tm_cv);
-        for (int s = 0; s < Z::NS + Z::NQ; ++s) mbar_init(barP + 8 * s, 1);
+        for (int s = 0; s < Z::NBAR; ++s) mbar_init(fullP + 8 * s, 1);
         fence_barrier_init();
     }
     __syncthreads();
 
-    uint32_t phP = 0, phQ = 0;
-    unsigned qissue = 0, qcons = 0;
-    __shared__ int s_item;
+    if (tid >= Z::NC) {
+        // ---- producer warp
+        const int lane = tid - Z::NC;
+        if (lane == 0) {  // items + the p_cur ring
+            uint32_t peP = 0, peI = 0;
+            int slot = 0;
+            for (int n = 0;; ++n) {
+                const int item = atomicAdd(P.wq.ctr, 1);
+                const int si = n % Z::NI;
+                const uint32_t par = ((peI >> si) & 1u) ^ 1u;
+                mbar_wait_sleep(emptyI + 8 * si, par);
+                mbar_wait_sleep(emptyS + 8 * si, par);
+                peI ^= 1u << si;
+                const int4 sg = item < P.wq.nitems ? P.segs[item] : make_int4(-1, 0, 0, 0);
+                items[si] = sg;
+                mbar_arrive_b(fullI + 8 * si);
+                mbar_arrive_b(fullS + 8 * si);
+                if (sg.x < 0) break;
+                const int x0 = P.x_base + sg.x * C::TX, y0 = P.lo[1] + sg.y * C::TY;
+                const int nring = sg.w - sg.z + 2 * R;
+                for (int j = 0; j < nring; ++j) {
+                    mbar_wait_sleep(emptyP + 8 * slot, ((peP >> slot) & 1u) ^ 1u);
+                    peP ^= 1u << slot;
+                    const uint32_t bar = fullP + 8 * slot;
+                    mbar_expect_tx(bar, C::BX * C::BY * 4);
+                    tma_load_3d(smem_u32(ring + slot * C::PLANE), &tm_pc, L.L + x0 - C::HX,
+                                y0 - R + L.r, sg.z - R + j + L.r, bar);
+                    slot = slot + 1 == Z::NS ? 0 : slot + 1;
+                }
+            }
+        } else if (lane == 1) {  // p_prev / c stages
+            uint32_t peQ = 0, phS = 0;
+            int st = 0;
+            for (int n = 0;; ++n) {
+                const int si = n % Z::NI;
+                mbar_wait_sleep(fullS + 8 * si, (phS >> si) & 1u);
+                phS ^= 1u << si;
+                const int4 sg = items[si];
+                mbar_arrive_b(emptyS + 8 * si);
+                if (sg.x < 0) break;
+                const int tmx = L.L + P.x_base + sg.x * C::TX, tmy = P.lo[1] + sg.y * C::TY + L.r;
+                for (int z = sg.z; z < sg.w; ++z) {
+                    mbar_wait_sleep(emptyQ + 8 * st, ((peQ >> st) & 1u) ^ 1u);
+                    peQ ^= 1u << st;
+                    const uint32_t bar = fullQ + 8 * st;
+                    float* dst = qring + st * 2 * C::TILE;
+                    mbar_expect_tx(bar, 2 * C::TX * C::TY * 4);
+                    tma_load_3d(smem_u32(dst), &tm_pp, tmx, tmy, z + L.r, bar);
+                    tma_load_3d(smem_u32(dst + C::TILE), &tm_cv, tmx, tmy, z + L.r, bar);
+                    st = st + 1 == Z::NQ ? 0 : st + 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers
+    const int tx = tid % C::TXT, ty = tid / C::TXT;
     const int soff = (R + ty) * C::BX + C::HX + 4 * tx;
     const int toff = ty * C::TX + 4 * tx;
+    uint32_t phP = 0, phQ = 0, phI = 0;
+    int cslot = 0, cst = 0;
+    auto csync = [] { asm volatile("bar.sync 1, %0;" ::"n"(Z::NC) : "memory"); };
 
-    for (;;) {
-        const int item = wq_next(P.wq, &s_item);
-        if (item >= P.wq.nitems) break;
-        const int4 sg = P.segs[item];
+    for (int n = 0;; ++n) {
+        const int si = n % Z::NI;
+        mbar_wait(fullI + 8 * si, (phI >> si) & 1u);
+        phI ^= 1u << si;
+        const int4 sg = items[si];
+        csync();  // every consumer has read the item
+        if (tid == 0) mbar_arrive_b(emptyI + 8 * si);
+        if (sg.x < 0) break;
         const int x0 = P.x_base + sg.x * C::TX;
         const int y0 = P.lo[1] + sg.y * C::TY;
         const int zb = sg.z, ze = sg.w;
         const int nring = ze - zb + 2 * R;
         const int nout = ze - zb;
-        const int tmx_halo = L.L + x0 - C::HX, tmy_halo = y0 - R + L.r;
-        const int tmx = L.L + x0, tmy = y0 + L.r;
-        auto issue_p = [&](int j, int slot) {
-            const uint32_t bar = barP + 8 * slot;
-            mbar_expect_tx(bar, C::BX * C::BY * 4);
-            tma_load_3d(smem_u32(ring + slot * C::PLANE), &tm_pc, tmx_halo, tmy_halo,
-                        zb - R + j + L.r, bar);
-        };
-        auto issue_q = [&](int o) {
-            const int st = qissue % Z::NQ;
-            const uint32_t bar = barQ + 8 * st;
-            float* dst = qring + st * 2 * C::TILE;
-            mbar_expect_tx(bar, 2 * C::TX * C::TY * 4);
-            tma_load_3d(smem_u32(dst), &tm_pp, tmx, tmy, zb + o + L.r, bar);
-            tma_load_3d(smem_u32(dst + C::TILE), &tm_cv, tmx, tmy, zb + o + L.r, bar);
-            ++qissue;
-        };
-        if (tid == 0) {
-            for (int j = 0; j < min(Z::NS, nring); ++j) issue_p(j, j);
-            for (int o = 0; o < min(Z::NQ, nout); ++o) issue_q(o);
-        }
 
         const int xg = x0 + 4 * tx;
         const int y = y0 + ty;
@@ -364,36 +419,43 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, 1)
             azb = __ldg(P.tb_z + z);
             azk = __ldg(P.tik_z + z);
         };
-        float4 nx_zz, nx_dz;
-        float nx_a, nx_b, nx_k;
+        float4 nx_zz = make_float4(0.f, 0.f, 0.f, 0.f), nx_dz = nx_zz;
+        float nx_a = 0.f, nx_b = 1.f, nx_k = 1.f;
         if (nout > 0) load_cpml(0, nx_zz, nx_dz, nx_a, nx_b, nx_k);
 
-        int slot = 0;  // ring slot of plane j (j mod NS)
+        // slot offsets (floats) of planes j-2R .. j, oldest first
+        int so[2 * R + 1];
+#pragma unroll
+        for (int i = 0; i <= 2 * R; ++i) so[i] = 0;
+        int rslot = cslot;  // oldest ring slot not yet released
+        const float* ringT = ring + soff;
+        auto px = [](const float* v, int h, int m) {
+            return f2(v[C::HX + 2 * h + m], v[C::HX + 2 * h + 1 + m]);
+        };
 #pragma unroll 1
         for (int j = 0; j < nring; ++j) {
-            mbar_wait(barP + 8 * slot, (phP >> slot) & 1u);
+            const int slot = cslot;
+            cslot = cslot + 1 == Z::NS ? 0 : cslot + 1;
+            mbar_wait(fullP + 8 * slot, (phP >> slot) & 1u);
             phP ^= 1u << slot;
+#pragma unroll
+            for (int i = 0; i < 2 * R; ++i) so[i] = so[i + 1];
+            so[2 * R] = slot * C::PLANE;
+            int st = -1;
             if (j >= 2 * R) {
                 const int o = j - 2 * R;
                 const int z = zb + o;
                 const int zr = zrun_at(z);
                 float* zz_p = zr >= 0 ? P.zrun[zr].zeta + run_off(P.zrun[zr], 2, xg, y, z) : nullptr;
-                const float4 zz = nx_zz, dz = nx_dz;
+                const float4 zz4 = nx_zz, dz4 = nx_dz;
                 const float aza = nx_a, azb = nx_b, azk = nx_k;
                 if (o + 1 < nout) load_cpml(o + 1, nx_zz, nx_dz, nx_a, nx_b, nx_k);
-                int cu = slot - R;  // slot of the centre plane j - R
-                if (cu < 0) cu += Z::NS;
-                auto slot_of = [&](int m) {
-                    int t = cu + m;
-                    if (t >= Z::NS) t -= Z::NS;
-                    if (t < 0) t += Z::NS;
-                    return t;
-                };
-                const float* S = ring + cu * C::PLANE + soff;
-                const int st = qcons % Z::NQ;
-                mbar_wait(barQ + 8 * st, (phQ >> st) & 1u);
+                st = cst;
+                cst = cst + 1 == Z::NQ ? 0 : cst + 1;
+                mbar_wait(fullQ + 8 * st, (phQ >> st) & 1u);
                 phQ ^= 1u << st;
                 const float* Qp = qring + st * 2 * C::TILE + toff;
+                const float* S = ringT + so[R];  // centre plane j - R
                 float xs[4 + 2 * C::HX];
 #pragma unroll
                 for (int h = 0; h < (4 + 2 * C::HX) / 4; ++h) {
@@ -403,73 +465,101 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, 1)
                     xs[4 * h + 2] = v.z;
                     xs[4 * h + 3] = v.w;
                 }
-                float two_p0[4], d2x[4] = {0.f, 0.f, 0.f, 0.f}, d2y[4] = {0.f, 0.f, 0.f, 0.f},
-                                 d2z[4] = {0.f, 0.f, 0.f, 0.f};
+                F2 two_p0[2], d2x[2], d2y[2], d2z[2];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) two_p0[e] = 2.0f * xs[C::HX + e];
+                for (int h = 0; h < 2; ++h) {
+                    const F2 c = px(xs, h, 0);
+                    two_p0[h] = fa2<OC>(c, c);  // T(2) * c (exact)
+                    d2x[h] = d2y[h] = d2z[h] = f2zero();
+                }
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        d2x[e] = d2_term<OC>(d2x[e], P.cx[m - 1], xs[C::HX + e + m],
-                                             xs[C::HX + e - m], two_p0[e]);
+                    for (int h = 0; h < 2; ++h)
+                        d2x[h] = d2_term2<OC>(d2x[h], P.cx[m - 1], px(xs, h, m), px(xs, h, -m),
+                                              two_p0[h]);
 #pragma unroll
                 for (int m = 1; m <= R; ++m) {
-                    const float4 u = lds4(S + m * C::BX), d = lds4(S - m * C::BX);
+                    F2 u[2], d[2];
+                    lds4x2(S + m * C::BX, u[0], u[1]);
+                    lds4x2(S - m * C::BX, d[0], d[1]);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        d2y[e] = d2_term<OC>(d2y[e], P.cy[m - 1], comp(u, e), comp(d, e), two_p0[e]);
+                    for (int h = 0; h < 2; ++h)
+                        d2y[h] = d2_term2<OC>(d2y[h], P.cy[m - 1], u[h], d[h], two_p0[h]);
                 }
 #pragma unroll
                 for (int m = 1; m <= R; ++m) {
-                    const float4 u = lds4(ring + slot_of(m) * C::PLANE + soff);
-                    const float4 d = lds4(ring + slot_of(-m) * C::PLANE + soff);
+                    F2 u[2], d[2];
+                    lds4x2(ringT + so[R + m], u[0], u[1]);
+                    lds4x2(ringT + so[R - m], d[0], d[1]);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        d2z[e] = d2_term<OC>(d2z[e], P.cz[m - 1], comp(u, e), comp(d, e), two_p0[e]);
+                    for (int h = 0; h < 2; ++h)
+                        d2z[h] = d2_term2<OC>(d2z[h], P.cz[m - 1], u[h], d[h], two_p0[h]);
                 }
-                const float4 pp = lds4(Qp);
-                const float4 cv = lds4(Qp + C::TILE);
-                float out[4], nzz[4];
+                F2 pp[2], cv[2];
+                lds4x2(Qp, pp[0], pp[1]);
+                lds4x2(Qp + C::TILE, cv[0], cv[1]);
+                float out[4];
                 if (z >= P.zi_lo && z < P.zi_hi) {  // inner plane (update_plain)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        out[e] = acc<OC>(fs<OC>(two_p0[e], comp(pp, e)), comp(cv, e),
-                                         fa<OC>(fa<OC>(d2x[e], d2y[e]), d2z[e]));
+                    for (int h = 0; h < 2; ++h) {
+                        const F2 lap = fa2<OC>(fa2<OC>(d2x[h], d2y[h]), d2z[h]);
+                        float c0, c1;
+                        unf2(cv[h], c0, c1);
+                        unf2(fa2<OC>(fs2<OC>(two_p0[h], pp[h]), fm2v<OC>(c0, c1, lap)),
+                             out[2 * h], out[2 * h + 1]);
+                    }
                     if (yok) st4(dst_base + (long long)o * L.plane, out, pok, pall);
                 } else {
+                    const F2 zz[2] = {f2(zz4.x, zz4.y), f2(zz4.z, zz4.w)};
+                    const F2 dz[2] = {f2(dz4.x, dz4.y), f2(dz4.z, dz4.w)};
+                    float nzz[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float drx = acc<OC>(0.0f, d2x[e], ikx[e]);
-                    const float dry = acc<OC>(0.0f, d2y[e], iky);
-                    const float drz = acc<OC>(comp(dz, e), d2z[e], azk);
-                    nzz[e] = zr >= 0 ? acc<OC>(fm<OC>(aza, drz), azb, comp(zz, e)) : 0.0f;
-                    const float lap = fa<OC>(fa<OC>(fa<OC>(drx, 0.0f), fa<OC>(dry, 0.0f)),
-                                             fa<OC>(drz, nzz[e]));
-                    out[e] = acc<OC>(fs<OC>(two_p0[e], comp(pp, e)), comp(cv, e), lap);
+                    for (int h = 0; h < 2; ++h) {
+                        // drive = d2p * ik + dpsi (dpsi_x, dpsi_y and zeta_x/y are 0 here)
+                        const F2 drx = fa2<OC>(fm2v<OC>(ikx[2 * h], ikx[2 * h + 1], d2x[h]), f2zero());
+                        const F2 dry = fa2<OC>(fm2<OC>(iky, d2y[h]), f2zero());
+                        const F2 drz = fa2<OC>(fm2<OC>(azk, d2z[h]), dz[h]);
+                        const F2 nz =
+                            zr >= 0 ? fa2<OC>(fm2<OC>(aza, drz), fm2<OC>(azb, zz[h])) : f2zero();
+                        unf2(nz, nzz[2 * h], nzz[2 * h + 1]);
+                        const F2 lap = fa2<OC>(fa2<OC>(fa2<OC>(drx, f2zero()), fa2<OC>(dry, f2zero())),
+                                               fa2<OC>(drz, nz));
+                        float c0, c1;
+                        unf2(cv[h], c0, c1);
+                        unf2(fa2<OC>(fs2<OC>(two_p0[h], pp[h]), fm2v<OC>(c0, c1, lap)),
+                             out[2 * h], out[2 * h + 1]);
+                    }
+                    if (yok) {
+                        st4(dst_base + (long long)o * L.plane, out, pok, pall);
+                        if (zr >= 0) st4(zz_p, nzz, pok, pall);
+                    }
                 }
-                if (yok) {
-                    st4(dst_base + (long long)o * L.plane, out, pok, pall);
-                    if (zr >= 0) st4(zz_p, nzz, pok, pall);
-                }
-                }
-                ++qcons;
             }
-            __syncthreads();  // all threads are done with plane j-2R and stage o
-            if (tid == 0 && j >= 2 * R) {
-                const int jf = j - 2 * R + Z::NS;  // refill plane j-2R's slot
-                if (jf < nring) {
-                    int fs_ = slot - 2 * R;
-                    if (fs_ < 0) fs_ += Z::NS;
-                    issue_p(jf, fs_);
+            csync();  // all consumers are done with plane j - 2R and stage st
+            if (tid == 0) {
+                if (j >= 2 * R) {
+                    mbar_arrive_b(emptyP + 8 * rslot);
+                    rslot = rslot + 1 == Z::NS ? 0 : rslot + 1;
                 }
-                if (j - 2 * R + Z::NQ < nout) issue_q(j - 2 * R + Z::NQ);
+                if (st >= 0) mbar_arrive_b(emptyQ + 8 * st);
             }
-            if (++slot == Z::NS) slot = 0;
         }
-        qissue = qcons;
+        // the item's last 2R ring planes
+        if (tid == 0)
+            for (int k = 0; k < min(2 * R, nring); ++k) {
+                mbar_arrive_b(emptyP + 8 * rslot);
+                rslot = rslot + 1 == Z::NS ? 0 : rslot + 1;
+            }
     }
-    wq_done(P.wq);
+    // last CTA out resets the work counter
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(P.wq.ctr + 1, 1) == (int)gridDim.x - 1) {
+            atomicExch(P.wq.ctr, 0);
+            atomicExch(P.wq.ctr + 1, 0);
+        }
+    }
 }
 
 }  // namespace fast

@@ -11,13 +11,13 @@
 //  * legal cuts (nd + r <= cut <= n - nd - r) keep every CPML memory read
 //    inside its rank, so only p is exchanged, as in the reference;
 //  * one step (the "overlap" schedule):
-//      CPML pass 1 (all planes) -> p_next on the r planes next to each cut
-//      (+ the source when it sits there) -> ncclSend/ncclRecv of those planes
-//      into the neighbours' p_next ghost planes on a communication stream
-//      || the interior planes (interior kernel beside the boundary kernel)
-//      -> join -> epilogue (source, free surface on rank 0, receivers, the
-//      rank's finiteness check at its slab centre, dist.cpp:222-224) ->
-//      rotate.
+//      CPML pass 1 (all planes) -> [edge stream] p_next on the r planes next
+//      to each cut (+ the source when it sits there) -> [comm stream]
+//      ncclSend/ncclRecv of those planes into the neighbours' p_next ghost
+//      planes || [engine stream] the interior planes (interior kernel beside
+//      the boundary kernel) -> join -> epilogue (source, free surface on
+//      rank 0, receivers, the rank's finiteness check at its slab centre,
+//      dist.cpp:222-224) -> rotate.
 //    The exchanged planes become the neighbours' p_cur ghosts after the
 //    rotation: what the reference's exchange_halos(p_cur) produces before the
 //    next step, so the slabs are bit-identical to one engine on the whole
@@ -100,7 +100,8 @@ struct mm_cd_group {
     int z0 = 0, nz = 0;
     ncclComm_t comm = nullptr;
     cudaStream_t cs = nullptr;  // communication stream
-    cudaEvent_t ev_edges = nullptr, ev_comm = nullptr;
+    cudaStream_t es = nullptr;  // edge-plane stream
+    cudaEvent_t ev_p1 = nullptr, ev_edges = nullptr, ev_comm = nullptr;
     bool lower = false, upper = false;  // neighbours below / above
     int edges[4] = {0, 0, 0, 0};        // plane ranges next to the cuts
     int nedge = 0;
@@ -116,6 +117,11 @@ struct mm_cd_group {
             cudaStreamSynchronize(cs);
             cudaStreamDestroy(cs);
         }
+        if (es) {
+            cudaStreamSynchronize(es);
+            cudaStreamDestroy(es);
+        }
+        if (ev_p1) cudaEventDestroy(ev_p1);
         if (ev_edges) cudaEventDestroy(ev_edges);
         if (ev_comm) cudaEventDestroy(ev_comm);
         if (comm) mmb::nccl().CommDestroy(comm);
@@ -148,11 +154,21 @@ struct mm_cd_group {
         const StepParams sp = E.params();
         const bool fst = E.mode != MM_MODE_STRICT && E.fast;
         E.pass1();
-        if (nedge) E.update_ranges(edges, nedge);
+        // the planes next to the cuts on their own stream, issued first (the
+        // persistent interior kernels then fill the SMs they leave), so the
+        // transfer waits for them only, not for the interior
         const bool src_edge = in_edges(so);
-        if (src_edge) launch_inject(sp.pn, sp.cv, so, amp, amp_dev, step_dev, E.stream);
+        MM_CUDA(cudaEventRecord(ev_p1, E.stream));
+        MM_CUDA(cudaStreamWaitEvent(es, ev_p1, 0));
+        if (nedge) {
+            if (fst)
+                E.fast->update_ranges(sp, edges, nedge, es);
+            else
+                for (int i = 0; i < nedge; ++i) strict_update(sp, 0, edges[2 * i], edges[2 * i + 1], es);
+        }
+        if (src_edge) launch_inject(sp.pn, sp.cv, so, amp, amp_dev, step_dev, es);
         // halo planes of p_next: owned edge planes -> the neighbours' ghosts
-        MM_CUDA(cudaEventRecord(ev_edges, E.stream));
+        MM_CUDA(cudaEventRecord(ev_edges, es));
         MM_CUDA(cudaStreamWaitEvent(cs, ev_edges, 0));
         const int r = E.lay.r;
         const size_t count = (size_t)r * E.lay.plane;
@@ -182,6 +198,7 @@ struct mm_cd_group {
             else
                 E.update(0, ilo, ihi);
         }
+        MM_CUDA(cudaStreamWaitEvent(E.stream, ev_edges, 0));
         MM_CUDA(cudaStreamWaitEvent(E.stream, ev_comm, 0));
         Epilogue ep;
         std::memset(&ep, 0, sizeof ep);
@@ -262,6 +279,8 @@ int mm_cd_group_create(const mm_grid* global, const int* cuts, int world, int ra
     if (rc) return rc;
     MM_CUDA(cudaSetDevice(device));
     MM_CUDA(cudaStreamCreateWithFlags(&g->cs, cudaStreamNonBlocking));
+    MM_CUDA(cudaStreamCreateWithFlags(&g->es, cudaStreamNonBlocking));
+    MM_CUDA(cudaEventCreateWithFlags(&g->ev_p1, cudaEventDisableTiming));
     MM_CUDA(cudaEventCreateWithFlags(&g->ev_edges, cudaEventDisableTiming));
     MM_CUDA(cudaEventCreateWithFlags(&g->ev_comm, cudaEventDisableTiming));
     g->lower = rank > 0;

@@ -252,6 +252,7 @@ public:
         // instruction cache; the column kernel (smem z window) serves the inner
         // box and the Z slabs instead
         col_inner_ = kZs && R > 4;
+        if (R > 4 && tuning("wide_inner") >= 0) col_inner_ = kZs && tuning("wide_inner") == 0;
         if (col_inner_ && zm < 0) zmode_ = 2;
         cudaDeviceProp prop;
         MM_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -593,6 +594,9 @@ private:
         return w;
     }
 
+    // k_zslab runs one CTA per SM
+    int zs_ctas(const Work& w) const { return std::max(1, std::min(w.nitems, sms_)); }
+
     void launch_inner(const StepParams& p, int z_lo, int z_hi, int mode, cudaStream_t s) {
         launch_inner(p, ZRanges{{z_lo, z_hi}}, mode, s);
     }
@@ -643,9 +647,9 @@ private:
             if constexpr (kZs) {
                 constexpr size_t zsm = ZSlabCfg<R>::SMEM;
                 if (order_ == 2)
-                    k_zslab<R, 2><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+                    k_zslab<R, 2><<<zs_ctas(w), ZSlabCfg<R>::NT, zsm, s>>>(a, b, cv_in_, ip);
                 else
-                    k_zslab<R, 1><<<w.ctas, IC::NT, zsm, s>>>(a, b, cv_in_, ip);
+                    k_zslab<R, 1><<<zs_ctas(w), ZSlabCfg<R>::NT, zsm, s>>>(a, b, cv_in_, ip);
             }
         } else if (order_ == 2) {
             k_inner<R, 2><<<std::min(w.ctas, inner_cap_), IC::NT, IC::SMEM, s>>>(a, b, cv_in_, ip);
