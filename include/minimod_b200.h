@@ -241,8 +241,9 @@ int mm_zslab_validate_cuts(const int* cuts, int world, int nz, int ndamping_z, i
 /* One rank's slab [cuts[rank], cuts[rank+1]) of the global grid: its engine
  * (vp_local: the ghosted z-fastest slice of the global model, the
  * reference's vp_local, dist.cpp:171-180), the halo plan and the NCCL
- * communicator (ncclCommInitRank: a collective over all ranks).  nccl_id may
- * be NULL for world == 1. */
+ * communicator (ncclCommInitRank: a collective over all ranks).  nccl_id
+ * NULL: no communicator (world == 1, or in-process ranks for
+ * mm_cd_group_step_local). */
 int mm_cd_group_create(const mm_grid* global, const int* cuts, int world, int rank,
                        const unsigned char nccl_id[128], const float* vp_local,
                        const mm_engine_options* opts, float dt, double vmax, int device, int mode,
@@ -259,6 +260,12 @@ int mm_cd_group_slab(mm_cd_group* g, int* z0, int* nz);
  * the owning rank injects), free surface (rank 0), rotation.  Asynchronous
  * on the engine stream. */
 int mm_cd_group_step(mm_cd_group* g, float amp, const int* src_global);
+/* Test hook: one step of the ranks 0 .. n-1 of one decomposition created in
+ * this process on one device without an NCCL id: the same schedule, with
+ * device-to-device copies of the edge planes in place of NCCL and the ranks'
+ * phases interleaved from this thread by stream events (no kernel waits on
+ * another). */
+int mm_cd_group_step_local(mm_cd_group** groups, int n, float amp, const int* src_global);
 /* nsteps group steps with device amplitudes, receiver recording into columns
  * [first_sample, ...) when record != 0 (the rank's own receivers), and the
  * reference's per-rank finiteness check of the slab centre every step

@@ -147,6 +147,7 @@ SIGNATURES = {
     "mm_cd_group_slab": [_P, _ip, _ip],
     "mm_cd_group_step": [_P, C.c_float, _ip],
     "mm_cd_group_run": [_P, _fp, C.c_int, _ip, C.c_int, C.c_int, _fp],
+    "mm_cd_group_step_local": [C.POINTER(_P), C.c_int, C.c_float, _ip],
     "mm_sim_config_default": [C.POINTER(mm_sim_config)],
     "mm_run": [C.POINTER(mm_sim_config), _fp, C.c_int, C.c_int, _fp, C.POINTER(mm_run_report)],
     # acoustic_iso (variable density)

@@ -145,10 +145,22 @@ struct mm_cd_group {
         return false;
     }
 
-    // One step of the overlap schedule (see the file comment).  amp_dev /
-    // step_dev: device wavelet + step counter (device loop) or null (host amp).
-    void step(float amp, long long so, const float* amp_dev, int* step_dev,
-              const mmb::RecParams* rec) {
+    // One step of the overlap schedule (see the file comment), in two phases
+    // so an in-process test can interleave several ranks (step_local):
+    //   phase 1: pass 1, the edge planes (edge stream), the halo transfer
+    //            (communication stream: NCCL, or `local_peers` copies);
+    //   phase 2: the interior planes, the join, the epilogue, the rotation.
+    // amp_dev / step_dev: device wavelet + step counter (device loop) or null.
+    struct StepArgs {
+        float amp;
+        long long so;
+        const float* amp_dev;
+        int* step_dev;
+        const mmb::RecParams* rec;
+    };
+    mm_cd_group** local_peers = nullptr;  // in-process ranks (tests), else NCCL
+
+    void phase1(const StepArgs& a) {
         using namespace mmb;
         mm_cd_engine& E = *e;
         const StepParams sp = E.params();
@@ -157,7 +169,6 @@ struct mm_cd_group {
         // the planes next to the cuts on their own stream, issued first (the
         // persistent interior kernels then fill the SMs they leave), so the
         // transfer waits for them only, not for the interior
-        const bool src_edge = in_edges(so);
         MM_CUDA(cudaEventRecord(ev_p1, E.stream));
         MM_CUDA(cudaStreamWaitEvent(es, ev_p1, 0));
         if (nedge) {
@@ -166,31 +177,50 @@ struct mm_cd_group {
             else
                 for (int i = 0; i < nedge; ++i) strict_update(sp, 0, edges[2 * i], edges[2 * i + 1], es);
         }
-        if (src_edge) launch_inject(sp.pn, sp.cv, so, amp, amp_dev, step_dev, es);
+        if (in_edges(a.so)) launch_inject(sp.pn, sp.cv, a.so, a.amp, a.amp_dev, a.step_dev, es);
         // halo planes of p_next: owned edge planes -> the neighbours' ghosts
         MM_CUDA(cudaEventRecord(ev_edges, es));
         MM_CUDA(cudaStreamWaitEvent(cs, ev_edges, 0));
         const int r = E.lay.r;
         const size_t count = (size_t)r * E.lay.plane;
         float* pn = E.p[E.in].ptr;
-        if (lower || upper) {
+        float* own_lo = pn + (long long)r * E.lay.plane;        // planes [0, r)
+        float* own_hi = pn + (long long)nz * E.lay.plane;       // planes [nz - r, nz)
+        if (local_peers) {
+            // in place of NCCL: write my edge planes into the neighbours' ghosts
+            if (lower) {
+                mm_cd_engine& D = *local_peers[rank - 1]->e;
+                float* dst = D.p[D.in].ptr + (long long)(local_peers[rank - 1]->nz + r) * D.lay.plane;
+                MM_CUDA(cudaMemcpyAsync(dst, own_lo, count * 4, cudaMemcpyDeviceToDevice, cs));
+            }
+            if (upper) {
+                mm_cd_engine& D = *local_peers[rank + 1]->e;
+                MM_CUDA(cudaMemcpyAsync(D.p[D.in].ptr, own_hi, count * 4, cudaMemcpyDeviceToDevice,
+                                        cs));
+            }
+        } else if (lower || upper) {
             const NcclApi& N = nccl();
             nccl_check(N.GroupStart(), "ncclGroupStart");
             if (lower) {
-                nccl_check(N.Send(pn + (long long)r * E.lay.plane, count, ncclFloat, rank - 1, comm, cs),
-                           "ncclSend");
+                nccl_check(N.Send(own_lo, count, ncclFloat, rank - 1, comm, cs), "ncclSend");
                 nccl_check(N.Recv(pn, count, ncclFloat, rank - 1, comm, cs), "ncclRecv");
             }
             if (upper) {
-                nccl_check(N.Send(pn + (long long)nz * E.lay.plane, count, ncclFloat, rank + 1, comm, cs),
-                           "ncclSend");
-                nccl_check(N.Recv(pn + (long long)(nz + r) * E.lay.plane, count, ncclFloat, rank + 1,
-                                  comm, cs),
+                nccl_check(N.Send(own_hi, count, ncclFloat, rank + 1, comm, cs), "ncclSend");
+                nccl_check(N.Recv(pn + (long long)(nz + r) * E.lay.plane, count, ncclFloat,
+                                  rank + 1, comm, cs),
                            "ncclRecv");
             }
             nccl_check(N.GroupEnd(), "ncclGroupEnd");
         }
         MM_CUDA(cudaEventRecord(ev_comm, cs));
+    }
+
+    void phase2(const StepArgs& a) {
+        using namespace mmb;
+        mm_cd_engine& E = *e;
+        const StepParams sp = E.params();
+        const bool fst = E.mode != MM_MODE_STRICT && E.fast;
         // the interior planes, concurrent with the transfer
         if (ihi > ilo) {
             if (fst)
@@ -200,23 +230,34 @@ struct mm_cd_group {
         }
         MM_CUDA(cudaStreamWaitEvent(E.stream, ev_edges, 0));
         MM_CUDA(cudaStreamWaitEvent(E.stream, ev_comm, 0));
+        if (local_peers) {  // the neighbours' copies into my ghosts
+            if (lower) MM_CUDA(cudaStreamWaitEvent(E.stream, local_peers[rank - 1]->ev_comm, 0));
+            if (upper) MM_CUDA(cudaStreamWaitEvent(E.stream, local_peers[rank + 1]->ev_comm, 0));
+        }
         Epilogue ep;
         std::memset(&ep, 0, sizeof ep);
         ep.p = sp.pn;
         ep.cv = sp.cv;
-        ep.src_off = src_edge ? -1LL : so;
-        ep.amp = amp;
-        ep.amp_dev = amp_dev;
-        ep.step_dev = step_dev;
-        ep.count = step_dev != nullptr;
+        ep.src_off = in_edges(a.so) ? -1LL : a.so;
+        ep.amp = a.amp;
+        ep.amp_dev = a.amp_dev;
+        ep.step_dev = a.step_dev;
+        ep.count = a.step_dev != nullptr;
         ep.fs = E.free_surface && E.goff[2] == 0;
         ep.lay = E.lay;
-        if (rec) ep.rec = *rec;
-        ep.check_off = rec && rec->bad_step ? centre : -1;
+        if (a.rec) ep.rec = *a.rec;
+        ep.check_off = a.rec && a.rec->bad_step ? centre : -1;
         ep.done = E.counters.ptr + 2;
         launch_epilogue(ep, E.stream);
         E.rotate();
         ++E.steps;
+    }
+
+    void step(float amp, long long so, const float* amp_dev, int* step_dev,
+              const mmb::RecParams* rec) {
+        const StepArgs a{amp, so, amp_dev, step_dev, rec};
+        phase1(a);
+        phase2(a);
     }
 };
 
@@ -303,8 +344,7 @@ int mm_cd_group_create(const mm_grid* global, const int* cuts, int world, int ra
     g->ilo = g->lower ? std::min(r, nz) : 0;
     g->ihi = g->upper ? std::max(nz - r, g->ilo) : nz;
     g->centre = g->e->lay.off(global->n[0] / 2, global->n[1] / 2, nz / 2);
-    if (world > 1 || nccl_id) {
-        need(nccl_id, "nccl_id");
+    if (nccl_id) {  // (world > 1 without an id: in-process ranks, mm_cd_group_step_local)
         ncclUniqueId u;
         std::memcpy(&u, nccl_id, sizeof u);
         nccl_check(nccl().CommInitRank(&g->comm, world, u, rank), "ncclCommInitRank");
@@ -339,8 +379,37 @@ int mm_cd_group_step(mm_cd_group* g, float amp, const int* src_global) {
     MM_API_BEGIN
     need(g, "group");
     MM_CUDA(cudaSetDevice(g->e->device));
-    if (g->world > 1 && !g->comm) raise(ST_NCCL, "group has no communicator");
+    if (g->world > 1 && !g->comm)
+        raise(ST_NCCL, "group has no communicator (in-process ranks step with mm_cd_group_step_local)");
     g->step(amp, g->local_src(src_global), nullptr, nullptr, nullptr);
+    MM_API_END
+}
+
+int mm_cd_group_step_local(mm_cd_group** groups, int n, float amp, const int* src_global) {
+    MM_API_BEGIN
+    need(groups, "groups");
+    if (n < 1) raise(ST_INVAL, "need at least one rank");
+    for (int i = 0; i < n; ++i) {
+        need(groups[i], "group");
+        if (groups[i]->world != n || groups[i]->rank != i)
+            raise(ST_INVAL, "groups must be the ranks 0 .. n-1 of one decomposition");
+        if (groups[i]->e->device != groups[0]->e->device)
+            raise(ST_INVAL, "in-process ranks share one device");
+    }
+    MM_CUDA(cudaSetDevice(groups[0]->e->device));
+    std::vector<mm_cd_group::StepArgs> args(n);
+    for (int i = 0; i < n; ++i) {
+        groups[i]->local_peers = groups;
+        args[i] = {amp, groups[i]->local_src(src_global), nullptr, nullptr, nullptr};
+    }
+    try {
+        for (int i = 0; i < n; ++i) groups[i]->phase1(args[i]);
+        for (int i = 0; i < n; ++i) groups[i]->phase2(args[i]);
+    } catch (...) {
+        for (int i = 0; i < n; ++i) groups[i]->local_peers = nullptr;
+        throw;
+    }
+    for (int i = 0; i < n; ++i) groups[i]->local_peers = nullptr;
     MM_API_END
 }
 
@@ -353,6 +422,7 @@ int mm_cd_group_run(mm_cd_group* g, const float* amps, int nsteps, const int* sr
     if (nsteps < 0) raise(ST_INVAL, "nsteps must be >= 0");
     if (nsteps == 0) return MM_OK;
     need(amps, "amps");
+    if (g->world > 1 && !g->comm) raise(ST_NCCL, "group has no communicator");
     const bool rec_on = record && e->nrec > 0;
     if (rec_on && (first_sample < 0 || first_sample + nsteps > e->cap))
         raise(ST_INVAL, "recorded steps exceed the trace capacity");

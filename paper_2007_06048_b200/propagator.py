@@ -377,6 +377,14 @@ class ZSlabGroup:
         return ms.value
 
 
+def step_local(groups, amp: float, src_global: Optional[Sequence[int]] = None):
+    """One step of in-process ranks (ZSlabGroup made without an NCCL id) on one
+    device: mm_cd_group_step_local (test hook; device-to-device halo copies)."""
+    arr = (C.c_void_p * len(groups))(*[g._h for g in groups])
+    check(lib().mm_cd_group_step_local(arr, len(groups), C.c_float(amp),
+                                       _i3(*src_global) if src_global is not None else None))
+
+
 class AcousticVdEngine:
     """Variable-density first-order acoustic propagator with CPML on the GPU.
 

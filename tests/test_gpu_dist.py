@@ -150,3 +150,37 @@ def test_group_nccl_world2_equals_single_engine(mm):
     full = one.pressure()[:, :, 4:-4]
     for _, rank, field in sorted(res, key=lambda t: t[1]):
         assert np.array_equal(field, full[:, :, cuts[rank]:cuts[rank + 1]]), rank
+
+
+@pytest.mark.parametrize("mode,fs,src_z,cuts", [
+    ("fast", False, 32, None),          # cost-weighted cuts, 3 ranks
+    ("fast", True, 25, [0, 27, 64]),    # source 2 planes below a cut (an edge plane)
+    ("strict", False, 40, [0, 22, 43, 64]),
+])
+def test_cpp_group_multirank_in_process_bitwise(mm, mode, fs, src_z, cuts):
+    """The C++ group schedule with several ranks (edge planes on their own
+    stream, halo transfer, interior, epilogue, rotation), ranks in one process
+    on one GPU through mm_cd_group_step_local (device-to-device copies in place
+    of NCCL): every slab equals one engine on the whole grid, bitwise."""
+    from paper_2007_06048_b200.propagator import ZSlabGroup, step_local
+    n, nd, steps, dt = (40, 36, 64), (5, 6, 7), 40, 1.2e-3
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0))
+    model = mm.random_model(grid, seed=5)
+    opts = mm.EngineOptions(ndamping=nd, taper=True, free_surface=fs)
+    w = mm.ricker(25.0, dt, steps).samples
+    src = (20, 18, src_z)
+    whole = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, dt, model.vmax, mode=mode)
+    for s in range(steps):
+        whole.step(float(w[s]), src)
+    full = whole.pressure()
+    cuts = cuts or D.weighted_cuts(n, nd, 4, 3)
+    D.validate_cuts(cuts, n[2], nd[2], 4)
+    groups = [ZSlabGroup(grid, cuts, r, model.vp, opts, dt, model.vmax, mode=mode)
+              for r in range(len(cuts) - 1)]
+    for s in range(steps):
+        step_local(groups, float(w[s]), src)
+    for g in groups:
+        got = g.engine.pressure()[:, :, 4:-4]
+        assert np.array_equal(got, full[:, :, 4 + g.z0:4 + g.z0 + g.nz]), (g.rank, cuts)
+    for g in groups:
+        g.close()
