@@ -62,15 +62,26 @@ def validate_cuts(cuts: Sequence[int], n: int, nd: int, radius: int) -> None:
             raise ConfigError(f"slab [{a}, {b}) is thinner than the stencil radius {radius}")
 
 
-def plane_costs(n: Sequence[int], nd: Sequence[int]) -> np.ndarray:
-    """Algorithmic bytes of each z plane under the byte model:
-    16 B per point + 16 B per damped axis of the point."""
+# Relative cost of a plane inside a z damping layer, measured on B200: every
+# rank's slab of 512^3 / 1000^3 timed alone (tools/scaling_projection.py,
+# profiles/r02_scaling_projection.json) gives 2.7-3.2x the time of an
+# undamped plane, against 1.9x in the byte model (the z runs' pass-1 chains
+# and the Z-slab tiles cost more than their bytes).
+ZDAMP_PLANE_WEIGHT = 3.1
+
+
+def plane_costs(n: Sequence[int], nd: Sequence[int], zdamp_weight: float = ZDAMP_PLANE_WEIGHT
+                ) -> np.ndarray:
+    """Relative cost of each z plane for the cuts: the byte model (BASELINE.md
+    2: 16 B per point + 16 B per damped axis) for the x/y damping, with a plane
+    of a z damping layer weighted `zdamp_weight` times an undamped plane
+    (measured; the byte model alone says ~1.9)."""
     nx, ny, nz = n
     dx = 2 * min(nd[0], nx) / nx
     dy = 2 * min(nd[1], ny) / ny
     z = np.arange(nz)
     zdamp = ((z < nd[2]) | (z >= nz - nd[2])).astype(np.float64)
-    per_point = 16.0 + 16.0 * (dx + dy + zdamp)
+    per_point = (16.0 + 16.0 * (dx + dy)) * (1.0 + (zdamp_weight - 1.0) * zdamp)
     return per_point * nx * ny
 
 
