@@ -26,9 +26,13 @@ namespace fast {
 
 // Z = true: the z-run items (2R+1-plane window, dpsi_z emission); Z = false:
 // the x- and y-run items, which need no window and run many more CTAs per SM.
+#ifndef MM_P1Z_TY
+#define MM_P1Z_TY 16
+#endif
+
 template <int R, bool Z>
 struct P1Cfg {
-    static constexpr int TX = 32, TY = 16;
+    static constexpr int TX = 32, TY = Z ? MM_P1Z_TY : 16;
     static constexpr int NC = (TX / 4) * TY;  // 128 consumer threads, float4 each
     static constexpr int NCW = NC / 32;
     static constexpr int NT = NC + 32;        // + producer warp

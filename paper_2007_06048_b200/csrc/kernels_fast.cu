@@ -203,8 +203,8 @@ public:
             in_tile_[b] = field_map(lay, bufs[b], IC::TX, IC::TY);
             bd_halo_[b] = field_map(lay, bufs[b], BC::BX, BC::BY);
             bd_tile_[b] = field_map(lay, bufs[b], BC::TX, BC::TY);
-            p1x_[b] = field_map(lay, bufs[b], P1C::BXX, P1C::TY);
-            p1y_[b] = field_map(lay, bufs[b], P1C::TX, P1C::BYY);
+            p1x_[b] = field_map(lay, bufs[b], P1X::BXX, P1X::TY);
+            p1y_[b] = field_map(lay, bufs[b], P1X::TX, P1X::BYY);
             p1z_[b] = field_map(lay, bufs[b], P1C::TX, P1C::TY);
             if constexpr (kCpml) {
                 cm_pc_[b] = field_map(lay, bufs[b], CC::BX, CC::BY);
@@ -699,7 +699,8 @@ private:
                 if (a == 0) maps_.psi[0][sd] = run_map(lay_, r, a, r.psi, BC::BX, BC::TY);  // x halo
                 if (a == 1) maps_.psi[1][sd] = run_map(lay_, r, a, r.psi, BC::TX, BC::BY);  // y halo
                 maps_.zeta[a][sd] = run_map(lay_, r, a, r.zeta, BC::TX, BC::TY);
-                p1maps_.psi[a][sd] = run_map(lay_, r, a, r.psi, P1C::TX, P1C::TY);
+                p1maps_.psi[a][sd] = a == 2 ? run_map(lay_, r, a, r.psi, P1C::TX, P1C::TY)
+                                            : run_map(lay_, r, a, r.psi, P1X::TX, P1X::TY);
                 if constexpr (kCpml) {
                     cmaps_.psi[a][sd] = run_map(lay_, r, a, r.psi, CC::TX, CC::TY);
                     cmaps_.zeta[a][sd] = run_map(lay_, r, a, r.zeta, CC::TX, CC::TY);
@@ -804,8 +805,9 @@ private:
                         d.x_base = d.lo[0] & ~3;  // = r.org for axis 0
                         const int ri = e.nrd++;
                         e.rd[ri] = d;
-                        const int tx = (d.hi[0] - d.x_base + P1C::TX - 1) / P1C::TX;
-                        const int ty = (d.hi[1] - d.lo[1] + P1C::TY - 1) / P1C::TY;
+                        const int TXa = ax == 2 ? P1C::TX : P1X::TX, TYa = ax == 2 ? P1C::TY : P1X::TY;
+                        const int tx = (d.hi[0] - d.x_base + TXa - 1) / TXa;
+                        const int ty = (d.hi[1] - d.lo[1] + TYa - 1) / TYa;
                         // z runs: one item spans the whole run (the dpsi_z window)
                         if (ax == 2 && (d.lo[2] != r.lo || d.hi[2] != r.hi))
                             raise(ST_INVAL, "pass 1 z range must not cut a z damping run");
