@@ -286,6 +286,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     kms = {k: v[0] / v[1] for k, v in kt.items() if v[1] > 0}
     klaunch = {k: int(v[1]) for k, v in kt.items()}
+    cpml_path = eng.cpml_path()
+    # one engine at a time: a second live engine in the process costs ~8 % per
+    # step (shared hardware queues), so the e2e engine gets the GPU to itself
+    eng.close()
+    del eng
+    torch.cuda.synchronize()
     # e2e through the public API with host buffers
     eng2 = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp,
                                mm.EngineOptions(ndamping=nd, taper=True), dt, model.vmax,
@@ -340,7 +346,7 @@ def run_ours(args):
                                   " (BASELINE configs[3] at N = 1)" if edge == 1000 else
                                   " (BASELINE configs[4] radius sweep)" if edge == 512 else ""),
                    "grid": list(n), "radius": r, "ndamping": list(nd), "mode": args.mode,
-                   "cpml_path": eng.cpml_path(),
+                   "cpml_path": cpml_path,
                    "flops_per_point": cost.flops_per_point,
                    "arithmetic_intensity": round(cost.arithmetic_intensity, 4),
                    "l2": "working set (3 p fields + c + CPML) > 126 MB L2; no flush"},

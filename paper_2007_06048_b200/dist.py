@@ -460,6 +460,16 @@ def bench_rank(args, rank, world, local):
     eng.synchronize()
     wall_ms = (time.perf_counter() - t0) * 1e3
     e2e_ms = _max(max(wall_ms, ms))
+    # host cost of issuing one group step (the C++ schedule: launches, events,
+    # the NCCL group), measured on the host clock without synchronising
+    dist.barrier()
+    nh = min(args.steps, 20)
+    h0 = time.perf_counter()
+    for s in range(nh):
+        grp.step(float(w[args.warmup + s]), src)
+    host_us = (time.perf_counter() - h0) * 1e6 / nh
+    eng.synchronize()
+    host_us = _max(host_us)
     pts = float(n[0]) * n[1] * n[2]
     value = pts * args.steps / (dev_ms * 1e-3) / 1e9
     e2e = pts * args.steps / (e2e_ms * 1e-3) / 1e9
@@ -503,6 +513,7 @@ def bench_rank(args, rank, world, local):
             "e2e": {"value": round(e2e, 3), "unit": "Gpoints/s", "h2d_bytes_per_step": 4 * world,
                     "d2h_bytes_per_step": 4 * nrec},
             "gpu_launches": all_launches,
+            "host_issue_us_per_step": round(host_us, 1),
             "clocks": clk,
         }
         if eff:
