@@ -70,6 +70,19 @@ constexpr bool kCpmlExpNoFp = false;
 #define MM_CPML_PX 4
 #endif
 
+// Producer waits: a plain mbarrier.try_wait loop (the instruction suspends
+// the thread in hardware) or a nanosleep back-off between polls.
+#ifndef MM_CPML_PROD_SLEEP
+#define MM_CPML_PROD_SLEEP 1
+#endif
+__device__ __forceinline__ void prod_wait(uint32_t bar, uint32_t parity) {
+#if MM_CPML_PROD_SLEEP
+    mbar_wait_sleep(bar, parity);
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
 template <int R>
 struct CpmlCfg {
     static_assert(R <= 4, "k_cpml: the 3R+1-plane window of wider stencils does not fit");
@@ -238,7 +251,7 @@ __device__ __forceinline__ void cpml_produce_ring(const CpmlMaps& M, const CpmlP
     for (int j = 0; j < nring; ++j) {
         const int slot = pslot;
         pslot = pslot + 1 == C::NS ? 0 : pslot + 1;
-        mbar_wait_sleep(B.emptyP + 8 * slot, ((peP >> slot) & 1u) ^ 1u);
+        prod_wait(B.emptyP + 8 * slot, ((peP >> slot) & 1u) ^ 1u);
         peP ^= 1u << slot;
         const uint32_t bar = B.fullP + 8 * slot;
         mbar_expect_tx(bar, 4u * C::BX * C::BY);
@@ -264,7 +277,7 @@ __device__ __forceinline__ void cpml_produce_stages(const CpmlMaps& M, const Cpm
     for (int z = zb; z < ze; ++z) {
         const int st = pstage;
         pstage = pstage + 1 == C::NQ ? 0 : pstage + 1;
-        mbar_wait_sleep(B.emptyQ + 8 * st, ((peQ >> st) & 1u) ^ 1u);
+        prod_wait(B.emptyQ + 8 * st, ((peQ >> st) & 1u) ^ 1u);
         peQ ^= 1u << st;
         const uint32_t bar = B.fullQ + 8 * st;
         float* dst = qbuf + st * C::SSIZE;
@@ -715,8 +728,8 @@ __global__ void __launch_bounds__(CpmlCfg<R>::NT, 1)
                 const int item = atomicAdd(P.wq.ctr, 1);
                 const int si = n % C::NI;
                 const uint32_t par = ((peI >> si) & 1u) ^ 1u;
-                mbar_wait_sleep(B.emptyI + 8 * si, par);
-                mbar_wait_sleep(B.emptyS + 8 * si, par);
+                prod_wait(B.emptyI + 8 * si, par);
+                prod_wait(B.emptyS + 8 * si, par);
                 peI ^= 1u << si;
                 int4 sg = make_int4(-1, 0, 0, 0);
                 if (item < P.wq.nitems) sg = P.items[item];
@@ -735,7 +748,7 @@ __global__ void __launch_bounds__(CpmlCfg<R>::NT, 1)
             int pstage = 0;
             for (int n = 0;; ++n) {
                 const int si = n % C::NI;
-                mbar_wait_sleep(B.fullS + 8 * si, (phS >> si) & 1u);
+                prod_wait(B.fullS + 8 * si, (phS >> si) & 1u);
                 phS ^= 1u << si;
                 const int4 sg = items[si];
                 mbar_arrive_b(B.emptyS + 8 * si);
