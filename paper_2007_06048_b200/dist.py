@@ -447,7 +447,8 @@ def bench_rank(args, rank, world, local):
     clk = clocks.stop()
     dev_ms = _max(ms)
     # e2e: step by step through the C ABI, host amplitude in, receiver plane out
-    host = (torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
+    host = (torch.empty((args.steps, nrec), dtype=torch.float32,
+                        pin_memory=torch.cuda.is_available()).numpy()
             if owns else None)
     dist.barrier()
     torch.cuda.synchronize()

@@ -204,3 +204,112 @@ def test_gloo_world2_nccl_id_broadcast():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert len(got[0]) == 128 and got[0] == got[1]
+
+
+# ------------------------------------------------------------ bench_rank plumbing
+class _FakeEngine:
+    def set_receivers(self, ijk, cap):
+        assert ijk.shape[1] == 3 and (ijk[:, 2] >= 0).all()
+        self.cap = cap
+
+    def record(self, s):
+        assert 0 <= s < self.cap
+
+    def copy_trace_step(self, s, out, asynchronous=False):
+        assert 0 <= s < self.cap and out.dtype == np.float32
+
+    def synchronize(self):
+        pass
+
+
+class _FakeGroup:
+    """Stands in for ZSlabGroup (the C++ group needs GPUs and NCCL)."""
+
+    def __init__(self, grid, cuts, rank, vp_global, opts, dt, vmax, *, nccl_id=None, device=0,
+                 mode="fast", vp_local=None):
+        assert len(cuts) == 3 and vp_local.shape[2] == cuts[rank + 1] - cuts[rank] + 8
+        assert nccl_id is not None and len(nccl_id) == 128
+        self.engine = _FakeEngine()
+
+    def run(self, amps, src, record=True, first_sample=0):
+        return 0.5 * len(amps)
+
+    def step(self, amp, src):
+        pass
+
+    def close(self):
+        pass
+
+
+def _bench_worker(rank, world, port, scaling, q):
+    import contextlib
+    import io
+    import types
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK="0")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2007_06048_b200 import dist as D
+    from paper_2007_06048_b200 import propagator as P
+    P.ZSlabGroup = _FakeGroup
+    torch.cuda.set_device = lambda *a, **k: None
+    torch.cuda.synchronize = lambda *a, **k: None
+    D._single_gpu_ms_per_step = lambda *a, **k: 1.0
+    args = types.SimpleNamespace(steps=4, warmup=3, grid=64 if scaling == "weak" else 100,
+                                 radius=4, mode="fast", scaling=scaling, efficiency=True)
+    out = io.StringIO()
+    with contextlib.redirect_stdout(out):
+        D.bench_rank(args, rank, world, 0)
+    q.put((rank, out.getvalue()))
+
+
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_rank_world2_plumbing(scaling):
+    """bench.py --gpus 2 (bench_rank) end to end on two gloo ranks with a
+    stand-in for the C++ group: NCCL-id broadcast, cuts, max-over-ranks
+    timing, e2e loop, strong-scaling efficiency, one JSON line on rank 0."""
+    import json
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, scaling, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[1].strip() == ""
+    line = json.loads(res[0].strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == scaling
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and "host_issue_us_per_step" in line
+    if scaling == "weak":
+        assert line["config"]["grid"] == [64, 64, 128]
+    else:
+        assert line["config"]["grid"] == [100, 100, 100]
+        # fake times: 1 GPU 1.0 ms/step, 2 ranks 0.5 ms/step -> 100 %
+        assert abs(line["parallel_efficiency"]["efficiency_pct"] - 100.0) < 1e-6
+
+
+def test_bench_spawns_ranks_without_torchrun():
+    """`bench.py --gpus 2` started without torchrun launches two ranks itself
+    (torch.distributed.run) -- here the reference arm, which runs on rank 0
+    only and needs no GPU."""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    from oracle.oracle import available
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--impl",
+                        "reference", "--steps", "2", "--warmup", "1", "--grid", "64"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["grid"] == [64, 64, 128]
