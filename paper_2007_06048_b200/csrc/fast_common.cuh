@@ -188,9 +188,13 @@ __device__ __forceinline__ float d2_term(float t, float c, float pp, float pm, f
 
 // ---- packed pairs of fp32 (Blackwell's f32x2 ALU: FADD2 / FFMA2)
 // add.rn.f32x2 / sub.rn.f32x2 round each lane like add.rn.f32, so ORD 2 stays
-// bit-identical.  Products stay scalar __fmul_rn in ORD 2: ptxas contracts a
-// mul.rn.f32x2 feeding an add.rn.f32x2 into FFMA2 even with explicit
-// rounding (checked in SASS), which would change the rounding.
+// bit-identical.  A packed product in ORD 2 is fma.rn.f32x2(c, x, -0): the
+// exact product plus -0, rounded once == mul.rn (+0 + -0 = +0, subnormals
+// kept).  The -0 comes from constant memory so ptxas cannot see it: with a
+// literal -0 it rewrites the FMA as a multiply and then contracts that
+// multiply with the following add into one FFMA2 (checked in SASS), which
+// changes the rounding; so does mul.rn.f32x2 followed by add.rn.f32x2.
+static __constant__ unsigned long long kNegZero2 = 0x8000000080000000ull;
 struct F2 {
     unsigned long long r;
 };
@@ -225,16 +229,38 @@ __device__ __forceinline__ F2 fs2(F2 a, F2 b) {
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
     return d;
 }
-// (c0, c1) * x lane-wise
+// (c0, c1) * x lane-wise, each lane rounded once
 template <int ORD>
 __device__ __forceinline__ F2 fm2v(float c0, float c1, F2 x) {
-    float a, b;
-    unf2(x, a, b);
-    return f2(fm<ORD>(c0, a), fm<ORD>(c1, b));
+    F2 d;
+    if constexpr (ORD == 2) {
+#ifdef MM_F2_SCALAR_MUL  // A/B build variant: two FMULs and a pack
+        float a, b;
+        unf2(x, a, b);
+        return f2(__fmul_rn(c0, a), __fmul_rn(c1, b));
+#endif
+        asm("fma.rn.f32x2 %0, %1, %2, %3;"
+            : "=l"(d.r)
+            : "l"(f2(c0, c1).r), "l"(x.r), "l"(kNegZero2));
+    } else {
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(f2(c0, c1).r), "l"(x.r));
+    }
+    return d;
 }
 template <int ORD>
 __device__ __forceinline__ F2 fm2(float c, F2 x) {
     return fm2v<ORD>(c, c, x);
+}
+// a * b lane-wise
+template <int ORD>
+__device__ __forceinline__ F2 fmul2(F2 a, F2 b) {
+    float a0, a1;
+    unf2(a, a0, a1);
+    return fm2v<ORD>(a0, a1, b);
+}
+// lanes (x, y) or (z, w) of a float4
+__device__ __forceinline__ F2 half2(const float4& v, int h) {
+    return h == 0 ? f2(v.x, v.y) : f2(v.z, v.w);
 }
 // t + c * x  (reference `t += c * x`)
 template <int ORD>

@@ -182,6 +182,33 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, InnerCfg<R>::MINB)
                     const float4 pp = lds4(Qp);
                     const float4 cv = lds4(Qp + C::TILE);
                     float out[4];
+#ifndef MM_INNER_SCALAR
+                    if constexpr (ORD == 2) {
+                        // lane pairs (x, x+1) = points (0,1) and (2,3): FADD2 /
+                        // FFMA2 with every lane rounded like the scalar code
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int e = 2 * h;
+                            const F2 two_p0 = fm2<ORD>(2.0f, f2(xs[C::HX + e], xs[C::HX + e + 1]));
+                            F2 tx_ = f2zero(), ty_ = f2zero(), tz_ = f2zero();
+#pragma unroll
+                            for (int m = 1; m <= R; ++m) {
+                                tx_ = d2_term2<ORD>(tx_, P.cx[m - 1],
+                                                    f2(xs[C::HX + e + m], xs[C::HX + e + 1 + m]),
+                                                    f2(xs[C::HX + e - m], xs[C::HX + e + 1 - m]),
+                                                    two_p0);
+                                ty_ = d2_term2<ORD>(ty_, P.cy[m - 1], half2(yu[m - 1], h),
+                                                    half2(yd[m - 1], h), two_p0);
+                                tz_ = d2_term2<ORD>(tz_, P.cz[m - 1], half2(q[(CU + m) % C::QW], h),
+                                                    half2(q[(CU + C::QW - m) % C::QW], h), two_p0);
+                            }
+                            const F2 lap = fa2<ORD>(fa2<ORD>(tx_, ty_), tz_);
+                            const F2 o2 = fa2<ORD>(fs2<ORD>(two_p0, half2(pp, h)),
+                                                   fmul2<ORD>(half2(cv, h), lap));
+                            unf2(o2, out[e], out[e + 1]);
+                        }
+                    } else
+#endif
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float p0 = xs[C::HX + e];
