@@ -268,6 +268,7 @@ struct mm_cd_engine {
         if (rec) ep.rec = *rec;
         ep.check_off = check_off;
         ep.done = counters.ptr + 2;
+        ep.pdl = fst && tuning("epi_pdl") != 0;
         launch_epilogue(ep, stream);
         if (te >= 0) fast->timer.end(te, stream);
         rotate();

@@ -44,6 +44,7 @@ const Tunable kTunables[] = {
     {"cpml_zt", 0},      // k_cpml planes per work item (0: automatic)
     {"overlap", 1},      // interior kernel on a side stream beside the CPML kernels
     {"pdl", 1},          // programmatic dependent launch of k_bnd after k_p1
+    {"epi_pdl", 0},      // (experiment) programmatic launch of the step epilogue behind the boundary kernel
     {"inner_late", 0},   // (experiment) issue the interior kernel after pass 1 (1) or the boundary (2)
     {"main_prio", 0},    // (experiment) step stream at the greatest priority
     {"debug_sync", 0},   // (diagnostics) synchronize after every kernel (1) or every step (2)

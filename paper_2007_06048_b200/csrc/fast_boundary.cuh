@@ -227,7 +227,12 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
                     mbar_arrive_b(fullI + 8 * si);
                     ++ni;
                 }
-                if (sg.w < 0) break;
+                if (sg.w < 0) {
+                    // the queue is empty: a programmatically launched successor
+                    // (the step epilogue) may start while the last items drain
+                    grid_dep_launch();
+                    break;
+                }
                 const TileCfg<R> T(P, sg);
                 for (int j = 0; j < T.nring; ++j) {
                     mbar_wait_sleep(emptyP + 8 * s, ph ^ 1);

@@ -273,6 +273,28 @@ __device__ __forceinline__ F2 acc2(F2 t, float c, F2 x) {
         return d;
     }
 }
+// t + (c0, c1) * x lane-wise
+template <int ORD>
+__device__ __forceinline__ F2 acc2v(F2 t, float c0, float c1, F2 x) {
+    if constexpr (ORD == 2) {
+        return fa2<ORD>(t, fm2v<ORD>(c0, c1, x));
+    } else {
+        F2 d;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.r) : "l"(x.r), "l"(f2(c0, c1).r), "l"(t.r));
+        return d;
+    }
+}
+// central_derivative_at term, both lanes: t += c * (pp - pm)
+template <int ORD>
+__device__ __forceinline__ F2 d1_term2(F2 t, float c, F2 pp, F2 pm) {
+    return acc2<ORD>(t, c, fs2<ORD>(pp, pm));
+}
+__device__ __forceinline__ float4 f4(F2 a, F2 b) {
+    float4 v;
+    unf2(a, v.x, v.y);
+    unf2(b, v.z, v.w);
+    return v;
+}
 // second_derivative_at term, both lanes: t += c * ((pp + pm) - 2 p0)
 template <int ORD>
 __device__ __forceinline__ F2 d2_term2(F2 t, float c, F2 pp, F2 pm, F2 two_p0) {

@@ -261,16 +261,14 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
             for (int k = 0; k <= 2 * R; ++k) zq[k] = make_float4(0.f, 0.f, 0.f, 0.f);
             float* dz_p = P.dpz[T.side] + x + (long long)y * run.s1;  // plane od = -R
             auto emit_dpz = [&]() {  // dpsi_z at queue centre (plane od)
-                float dz[4] = {0.f, 0.f, 0.f, 0.f};
+                F2 dz[2] = {f2zero(), f2zero()};  // lane pairs (x, x+1), (x+2, x+3)
 #pragma unroll
-                for (int m = 1; m <= R; ++m) {
-                    const float4 u4 = zq[R + m], d4 = zq[R - m];
-                    dz[0] = acc<ORD>(dz[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
-                    dz[1] = acc<ORD>(dz[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
-                    dz[2] = acc<ORD>(dz[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
-                    dz[3] = acc<ORD>(dz[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
-                }
-                store4(dz_p, make_float4(dz[0], dz[1], dz[2], dz[3]));
+                for (int m = 1; m <= R; ++m)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        dz[h] = d1_term2<ORD>(dz[h], c1[m - 1], half2(zq[R + m], h),
+                                              half2(zq[R - m], h));
+                store4(dz_p, f4(dz[0], dz[1]));
                 dz_p += run.s2;
             };
             int wo[2 * R + 1];     // p_cur slot offsets of planes j-2R .. j
@@ -290,14 +288,13 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                     // it is independent of this plane's psi (more ILP per plane)
                     if (o > 0) emit_dpz();
                     const float az = __ldg(P.ta[2] + z), bz = __ldg(P.tb[2] + z);
-                    float dp[4] = {0.f, 0.f, 0.f, 0.f};
+                    F2 dp[2] = {f2zero(), f2zero()};
 #pragma unroll
                     for (int m = 1; m <= R; ++m) {
                         const float4 u4 = lds4(ring + wo[R + m]), d4 = lds4(ring + wo[R - m]);
-                        dp[0] = acc<ORD>(dp[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
-                        dp[1] = acc<ORD>(dp[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
-                        dp[2] = acc<ORD>(dp[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
-                        dp[3] = acc<ORD>(dp[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            dp[h] = d1_term2<ORD>(dp[h], c1[m - 1], half2(u4, h), half2(d4, h));
                     }
                     const int st = nq % C::NQ;
                     mbar_wait(fullQ + 8 * st, (nq / C::NQ) & 1);
@@ -310,10 +307,8 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                     ++nq;
                     if (++rel == C::NS) rel = 0;
                     // reference: psi = b * psi + a * dp  (propagator_impl.hpp:118-120)
-                    v.x = acc<ORD>(fm<ORD>(az, dp[0]), bz, v.x);
-                    v.y = acc<ORD>(fm<ORD>(az, dp[1]), bz, v.y);
-                    v.z = acc<ORD>(fm<ORD>(az, dp[2]), bz, v.z);
-                    v.w = acc<ORD>(fm<ORD>(az, dp[3]), bz, v.w);
+                    v = f4(acc2<ORD>(fm2<ORD>(az, dp[0]), bz, half2(v, 0)),
+                           acc2<ORD>(fm2<ORD>(az, dp[1]), bz, half2(v, 1)));
                     store4(dst + (long long)o * zstep, v);
 #pragma unroll
                     for (int k = 0; k < 2 * R; ++k) zq[k] = zq[k + 1];
@@ -359,7 +354,7 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                     const int t = cs + m;
                     return t < 0 ? t + C::NS : t >= C::NS ? t - C::NS : t;
                 };
-                float dp[4] = {0.f, 0.f, 0.f, 0.f};
+                F2 dp[2] = {f2zero(), f2zero()};  // lane pairs (x, x+1), (x+2, x+3)
                 const float* S = ring + cs * C::PSLOT + poff;
                 if (ax == 0) {
                     constexpr int H = C::HX;
@@ -373,10 +368,12 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                         v[4 * h + 3] = t.w;
                     }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
+                    for (int h = 0; h < 2; ++h)
 #pragma unroll
                         for (int m = 1; m <= R; ++m)
-                            dp[e] = acc<ORD>(dp[e], c1[m - 1], fs<ORD>(v[H + e + m], v[H + e - m]));
+                            dp[h] = d1_term2<ORD>(dp[h], c1[m - 1],
+                                                  f2(v[H + 2 * h + m], v[H + 2 * h + 1 + m]),
+                                                  f2(v[H + 2 * h - m], v[H + 2 * h + 1 - m]));
                 } else {
 #pragma unroll
                     for (int m = 1; m <= R; ++m) {
@@ -384,10 +381,9 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                                                   : lds4(ring + slot_of(m) * C::PSLOT + poff);
                         const float4 d4 = ax == 1 ? lds4(S - m * C::TX)
                                                   : lds4(ring + slot_of(-m) * C::PSLOT + poff);
-                        dp[0] = acc<ORD>(dp[0], c1[m - 1], fs<ORD>(u4.x, d4.x));
-                        dp[1] = acc<ORD>(dp[1], c1[m - 1], fs<ORD>(u4.y, d4.y));
-                        dp[2] = acc<ORD>(dp[2], c1[m - 1], fs<ORD>(u4.z, d4.z));
-                        dp[3] = acc<ORD>(dp[3], c1[m - 1], fs<ORD>(u4.w, d4.w));
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            dp[h] = d1_term2<ORD>(dp[h], c1[m - 1], half2(u4, h), half2(d4, h));
                     }
                 }
                 const int st = nq % C::NQ;
@@ -397,10 +393,8 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                 if (lane == 0) mbar_arrive_b(emptyQ + 8 * st);
                 ++nq;
                 // reference: psi = b * psi + a * dp  (propagator_impl.hpp:118-120)
-                v.x = acc<ORD>(fm<ORD>(av[0], dp[0]), bv[0], v.x);
-                v.y = acc<ORD>(fm<ORD>(av[1], dp[1]), bv[1], v.y);
-                v.z = acc<ORD>(fm<ORD>(av[2], dp[2]), bv[2], v.z);
-                v.w = acc<ORD>(fm<ORD>(av[3], dp[3]), bv[3], v.w);
+                v = f4(acc2v<ORD>(fm2v<ORD>(av[0], av[1], dp[0]), bv[0], bv[1], half2(v, 0)),
+                       acc2v<ORD>(fm2v<ORD>(av[2], av[3], dp[1]), bv[2], bv[3], half2(v, 1)));
                 store4(dst + (long long)o * zstep, v);
                 // plane j - 2w has had its last use
                 __syncwarp();

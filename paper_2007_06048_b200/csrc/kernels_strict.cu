@@ -205,25 +205,30 @@ __global__ void k_step_counter(int* step_dev) { *step_dev += 1; }
 // another thread could read -- is made by the last block to finish, after
 // all reads.  That block also advances the step counter.
 __global__ void k_epilogue(Epilogue e) {
+    // Everything the update kernels do not write is read before
+    // griddepcontrol.wait (a no-op without a programmatic launch): the step
+    // counter and wavelet sample, c at the source, the receiver offsets.
     const int step = e.step_dev ? *e.step_dev : e.rec.step;
     const Layout& L = e.lay;
     const bool has_src = e.src_off >= 0;
-    float inj = 0.0f;
-    if (has_src) {
-        const float a = e.amp_dev ? e.amp_dev[step] : e.amp;
-        inj = __fadd_rn(e.p[e.src_off], __fmul_rn(e.cv[e.src_off], a));  // propagator_impl.hpp:166-169
-    }
-    auto value = [&](long long o) { return has_src && o == e.src_off ? inj : e.p[o]; };
+    const float a = has_src ? (e.amp_dev ? e.amp_dev[step] : e.amp) : 0.0f;
+    const float cs = has_src ? e.cv[e.src_off] : 0.0f;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int ex = L.n[0] + 2 * L.r;
     const long long nfs = e.fs ? (long long)ex * L.ey : 0;
+    const bool is_rec = t >= nfs && t - nfs < e.rec.nrec;
+    const long long roff = is_rec ? e.rec.offs[t - nfs] : 0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    float inj = 0.0f;
+    if (has_src) inj = __fadd_rn(e.p[e.src_off], __fmul_rn(cs, a));  // propagator_impl.hpp:166-169
+    auto value = [&](long long o) { return has_src && o == e.src_off ? inj : e.p[o]; };
     if (t < nfs) {  // cpml.hpp:103-111
         const int i = (int)(t % ex) - L.r, j = (int)(t / ex) - L.r;
         e.p[L.off(i, j, 0)] = 0.0f;
         for (int m = 1; m <= L.r; ++m) e.p[L.off(i, j, -m)] = -value(L.off(i, j, m));
-    } else if (t - nfs < e.rec.nrec) {
+    } else if (is_rec) {
         const int r = (int)(t - nfs);
-        const long long o = e.rec.offs[r];
+        const long long o = roff;
         const bool on_surface = e.fs && o / L.plane == L.r;  // local z = 0
         const float v = on_surface ? 0.0f : value(o);
         e.rec.traces[(long long)step * e.rec.nrec + r] = v;
@@ -353,7 +358,16 @@ void launch_epilogue(const Epilogue& ep, cudaStream_t s) {
     const long long work = nfs + ep.rec.nrec + (ep.check_off >= 0 ? 1 : 0);
     if (work == 0 && ep.src_off < 0 && !ep.count) return;
     const int blocks = (int)std::max<long long>((work + 255) / 256, 1);
-    k_epilogue<<<blocks, 256, 0, s>>>(ep);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = ep.pdl ? at : nullptr;
+    cfg.numAttrs = ep.pdl ? 1 : 0;
+    MM_CUDA(cudaLaunchKernelEx(&cfg, k_epilogue, ep));
     note_launches(1);
     MM_CUDA(cudaGetLastError());
 }

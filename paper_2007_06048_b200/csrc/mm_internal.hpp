@@ -262,6 +262,7 @@ struct Epilogue {
     RecParams rec;         // nrec = 0: no sampling (rec.p is ignored: p)
     long long check_off;   // >= 0: finiteness check of this point into rec.bad_step
     int* done;             // block ticket (zero between launches)
+    bool pdl;              // programmatic launch: may start while the kernel before drains
 };
 
 // ---- launchers (kernels_strict.cu)
