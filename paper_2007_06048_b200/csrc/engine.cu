@@ -54,7 +54,7 @@ const Tunable kTunables[] = {
     {"bnd_zt", 12},      // k_bnd planes per work item (target)
     {"p1_zt", 16},       // k_p1 planes per work item (target)
     {"zslabs", -1},      // Z slabs: -1 auto, 0 k_bnd tiles, 1 k_zslab after k_inner, 2 k_zslab columns
-    {"wide_inner", -1},  // r > 4 interior: -1 auto, 0 column kernel k_zslab, 1 register-queue k_inner
+    {"wide_inner", -1},  // r > 4 interior: -1 auto (2), 0 column kernel k_zslab, 1 unrolled k_inner, 2 k_innerw
     {"bnd_kinds", 7},    // (profiling) slab kinds k_bnd updates (bit mask X/Y/Z)
     {"bnd_ctas", 0},     // (diagnostics) cap on k_bnd CTAs (0: none)
     {"p1_axes", 7},      // (profiling) run axes k_p1 updates (bit mask)

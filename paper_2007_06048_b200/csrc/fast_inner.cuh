@@ -589,5 +589,221 @@ __global__ void __launch_bounds__(ZSlabCfg<R>::NT, 1)
     }
 }
 
+
+// ------------------------------------------------------------ wide stencils
+// k_innerw: the inner box for R > 4 (update_plain, propagator_impl.hpp:89-104).
+// k_inner's register queue needs its z loop unrolled 2R+1 deep so that every
+// queue index is static (19 k instructions at R = 8: instruction-cache bound);
+// the column kernel k_zslab keeps the z window in shared memory instead (38
+// LDS.128 per thread-plane at R = 8: shared-memory-bandwidth bound).  Here the
+// z window stays in registers: the z loop is unrolled U (4) planes deep and the
+// queue shifted by moves once per U planes (2R float4 moves), so the loop
+// body stays short; the x/y neighbours come
+// from the centre plane's halo in shared memory, which therefore stays
+// resident only from its arrival until it is the centre (R + 1 planes plus
+// TMA lead) instead of the whole 2R+1 window.  One CTA of 12 warps per SM
+// (64 x 24 tiles), registers up to 168 per thread.
+template <int R>
+struct InnerWCfg {
+    static constexpr int TXT = 16;               // thread columns, 4 x-points each
+    static constexpr int TX = 4 * TXT;           // 64
+#ifndef MM_INNERW_TY
+#define MM_INNERW_TY 24
+#endif
+    static constexpr int TY = MM_INNERW_TY;      // thread rows
+    static constexpr int NT = TXT * TY;          // 384 threads
+    static constexpr int HX = 8;                 // x halo in shared memory (2 float4)
+    static constexpr int BX = TX + 2 * HX;
+    static constexpr int BY = TY + 2 * R;
+#ifndef MM_INNERW_U
+#define MM_INNERW_U 4
+#endif
+    static constexpr int U = MM_INNERW_U;        // planes per register-queue shift
+#ifndef MM_INNERW_LEAD
+#define MM_INNERW_LEAD 3
+#endif
+    static constexpr int LEAD = MM_INNERW_LEAD;  // planes the TMA ring runs ahead
+    static constexpr int NS = R + 1 + LEAD;      // ring slots: centre .. newest + lead
+    static constexpr int NQ = 4;                 // p_prev / c stages
+    static constexpr int PLANE = pad32(BX * BY);
+    static constexpr int TILE = pad32(TX * TY);
+    static constexpr size_t SMEM =
+        sizeof(float) * (size_t)(NS * PLANE + NQ * 2 * TILE) + 8 * (NS + NQ) + 16;
+};
+
+template <int R, int ORD>
+__global__ void __launch_bounds__(InnerWCfg<R>::NT, 1)
+    k_innerw(const __grid_constant__ CUtensorMap tm_pc, const __grid_constant__ CUtensorMap tm_pp,
+             const __grid_constant__ CUtensorMap tm_cv, const InnerParams P) {
+    using C = InnerWCfg<R>;
+    static_assert(C::NS <= 32 && C::NQ <= 32, "parity bit masks");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    float* qring = ring + C::NS * C::PLANE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(qring + C::NQ * 2 * C::TILE);
+    const uint32_t barP = smem_u32(bars), barQ = smem_u32(bars + C::NS);
+    const int tid = threadIdx.x;
+    const int tx = tid % C::TXT, ty = tid / C::TXT;
+    const Layout L = P.lay;
+
+    if (tid == 0) {
+        prefetch_tmap(&tm_pc);
+        prefetch_tmap(&tm_pp);
+        prefetch_tmap(&tm_cv);
+        for (int s = 0; s < C::NS + C::NQ; ++s) mbar_init(barP + 8 * s, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    uint32_t phP = 0, phQ = 0;  // parity bit per ring slot / stage
+    unsigned qissue = 0, qcons = 0;
+    __shared__ int s_item;
+    const int soff = (R + ty) * C::BX + C::HX + 4 * tx;  // in a p_cur plane
+    const int toff = ty * C::TX + 4 * tx;                 // in a p_prev / c tile
+
+    for (;;) {
+        const int item = wq_next(P.wq, &s_item);
+        if (item >= P.wq.nitems) break;
+        const int4 sg = P.segs[item];
+        const int x0 = P.x_base + sg.x * C::TX;
+        const int y0 = P.lo[1] + sg.y * C::TY;
+        const int zb = sg.z, ze = sg.w;
+        const int nring = ze - zb + 2 * R;  // planes zb-R .. ze+R-1; plane j in slot j % NS
+        const int nout = ze - zb;
+        auto issue_p = [&](int j, int slot) {
+            const uint32_t bar = barP + 8 * slot;
+            mbar_expect_tx(bar, C::BX * C::BY * 4);
+            tma_load_3d(smem_u32(ring + slot * C::PLANE), &tm_pc, L.L + x0 - C::HX, y0 - R + L.r,
+                        zb - R + j + L.r, bar);
+        };
+        auto issue_q = [&](int o) {
+            const int st = qissue % C::NQ;
+            const uint32_t bar = barQ + 8 * st;
+            float* dst = qring + st * 2 * C::TILE;
+            mbar_expect_tx(bar, 2 * C::TX * C::TY * 4);
+            tma_load_3d(smem_u32(dst), &tm_pp, L.L + x0, y0 + L.r, zb + o + L.r, bar);
+            tma_load_3d(smem_u32(dst + C::TILE), &tm_cv, L.L + x0, y0 + L.r, zb + o + L.r, bar);
+            ++qissue;
+        };
+        if (tid == 0) {
+            for (int j = 0; j < min(C::NS, nring); ++j) issue_p(j, j);
+            for (int o = 0; o < min(C::NQ, nout); ++o) issue_q(o);
+        }
+
+        const int xg = x0 + 4 * tx;
+        const int y = y0 + ty;
+        bool xok[4];
+        bool xall = true;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            xok[e] = xg + e >= P.lo[0] && xg + e < P.hi[0];
+            xall = xall && xok[e];
+        }
+        const bool yok = y >= P.lo[1] && y < P.hi[1];
+        float* dst = P.pn + L.off(xg, y, zb);
+
+        // register queue: q[k] = this thread's points in plane jb - 2R + k for
+        // a block of U planes jb .. jb + U - 1 (static indices inside the
+        // block), shifted by U after it: 2R float4 moves per U planes
+        constexpr int U = C::U;
+        float4 q[2 * R + U];
+        int sj = 0;  // slot of plane j
+        int sc = 0;  // slot of plane j - R (the centre once j >= 2R)
+#pragma unroll 1
+        for (int jb = 0; jb < nring; jb += U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = jb + u;
+                if (j >= nring) break;
+                mbar_wait(barP + 8 * sj, (phP >> sj) & 1u);
+                phP ^= 1u << sj;
+                q[2 * R + u] = lds4(ring + sj * C::PLANE + soff);
+                if (j >= 2 * R) {
+                    const float* S = ring + sc * C::PLANE + soff;
+                    const int st = qcons % C::NQ;
+                    const float4 p0 = q[R + u];
+                    float xs[4 + 2 * C::HX];  // x - HX .. x + 3 + HX
+#pragma unroll
+                    for (int h = 0; h < C::HX / 4; ++h) {
+                        const float4 lft = lds4(S - C::HX + 4 * h);
+                        const float4 rgt = lds4(S + 4 + 4 * h);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            xs[4 * h + e] = comp(lft, e);
+                            xs[C::HX + 4 + 4 * h + e] = comp(rgt, e);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) xs[C::HX + e] = comp(p0, e);
+                    F2 two_p0[2], tx_[2], ty_[2], tz_[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        two_p0[h] = fm2<ORD>(2.0f, half2(p0, h));
+                        tx_[h] = ty_[h] = tz_[h] = f2zero();
+                    }
+                    // laplacian_at (stencil.hpp:70-82), every lane in the reference order
+#pragma unroll
+                    for (int m = 1; m <= R; ++m)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            tx_[h] = d2_term2<ORD>(
+                                tx_[h], P.cx[m - 1],
+                                f2(xs[C::HX + 2 * h + m], xs[C::HX + 2 * h + 1 + m]),
+                                f2(xs[C::HX + 2 * h - m], xs[C::HX + 2 * h + 1 - m]), two_p0[h]);
+#pragma unroll
+                    for (int m = 1; m <= R; ++m) {
+                        const float4 up = lds4(S + m * C::BX), dn = lds4(S - m * C::BX);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            ty_[h] = d2_term2<ORD>(ty_[h], P.cy[m - 1], half2(up, h), half2(dn, h),
+                                                   two_p0[h]);
+                    }
+#pragma unroll
+                    for (int m = 1; m <= R; ++m)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            tz_[h] = d2_term2<ORD>(tz_[h], P.cz[m - 1], half2(q[R + u + m], h),
+                                                   half2(q[R + u - m], h), two_p0[h]);
+                    mbar_wait(barQ + 8 * st, (phQ >> st) & 1u);
+                    phQ ^= 1u << st;
+                    const float* Qp = qring + st * 2 * C::TILE + toff;
+                    const float4 pp = lds4(Qp), cv = lds4(Qp + C::TILE);
+                    float out[4];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const F2 lap = fa2<ORD>(fa2<ORD>(tx_[h], ty_[h]), tz_[h]);
+                        const F2 o2 = fa2<ORD>(fs2<ORD>(two_p0[h], half2(pp, h)),
+                                               fmul2<ORD>(half2(cv, h), lap));
+                        unf2(o2, out[2 * h], out[2 * h + 1]);
+                    }
+                    ++qcons;
+                    if (yok) {
+                        float* d = dst + (long long)(j - 2 * R) * L.plane;
+                        if (xall) {
+                            *reinterpret_cast<float4*>(d) =
+                                make_float4(out[0], out[1], out[2], out[3]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (xok[e]) d[e] = out[e];
+                        }
+                    }
+                }
+                __syncthreads();  // plane j - R (slot sc) and stage st have had their last use
+                if (tid == 0) {
+                    if (j >= R && j - R + C::NS < nring) issue_p(j - R + C::NS, sc);
+                    if (j >= 2 * R && j - 2 * R + C::NQ < nout) issue_q(j - 2 * R + C::NQ);
+                }
+                if (j >= R && ++sc == C::NS) sc = 0;
+                if (++sj == C::NS) sj = 0;
+            }
+#pragma unroll
+            for (int k = 0; k < 2 * R; ++k) q[k] = q[k + U];
+        }
+        qissue = qcons;
+    }
+    wq_done(P.wq);
+}
+
 }  // namespace fast
 }  // namespace mmb

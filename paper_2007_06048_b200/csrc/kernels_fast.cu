@@ -189,6 +189,8 @@ class FastPlanR final : public FastPlan {
     using P1X = P1Cfg<R, false>;   // x and y runs
     static constexpr bool kBnd = BC::SMEM <= 227 * 1024;  // TMA boundary kernel fits
     static constexpr bool kZs = ZSlabCfg<R>::SMEM <= 227 * 1024;  // optional Z-slab kernel
+    using IW = InnerWCfg<R>;
+    static constexpr bool kW = R > 4 && IW::SMEM <= 227 * 1024;  // wide-stencil inner kernel
     static constexpr bool kP1 = P1C::SMEM <= 200 * 1024;
     static constexpr int RC = R <= 4 ? R : 4;  // (k_cpml is instantiated for R <= 4 only)
     using CC = CpmlCfg<RC>;
@@ -212,6 +214,13 @@ public:
             }
         }
         cv_in_ = field_map(lay, cv, IC::TX, IC::TY);
+        if constexpr (kW) {
+            for (int b = 0; b < 3; ++b) {
+                inw_halo_[b] = field_map(lay, bufs[b], IW::BX, IW::BY);
+                inw_tile_[b] = field_map(lay, bufs[b], IW::TX, IW::TY);
+            }
+            cv_inw_ = field_map(lay, cv, IW::TX, IW::TY);
+        }
         cv_bd_ = field_map(lay, cv, BC::TX, BC::TY);
         if constexpr (kCpml) cm_cv_ = field_map(lay, cv, CC::TX, CC::TY);
         // z-chunk targets (planes per work item) of the persistent kernels
@@ -248,11 +257,15 @@ public:
             MM_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
             MM_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
         }
-        // R > 4: the interior kernel's z loop unrolled by 2R+1 overflows the
-        // instruction cache; the column kernel (smem z window) serves the inner
-        // box and the Z slabs instead
-        col_inner_ = kZs && R > 4;
-        if (R > 4 && tuning("wide_inner") >= 0) col_inner_ = kZs && tuning("wide_inner") == 0;
+        // R > 4: k_inner's z loop unrolled by 2R+1 overflows the instruction
+        // cache; k_innerw (register queue rotated by moves) serves the inner box
+        // (tuning wide_inner: 0 = the column kernel k_zslab over the inner box
+        // and the Z slabs, 1 = k_inner, 2 = k_innerw)
+        if constexpr (R > 4) {
+            const long long wi = tuning("wide_inner");
+            wide_ = kW && (wi < 0 || wi == 2);
+            col_inner_ = kZs && !wide_ && wi != 1;
+        }
         if (col_inner_ && zm < 0) zmode_ = 2;
         cudaDeviceProp prop;
         MM_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -260,6 +273,10 @@ public:
         for (auto fn : {k_inner<R, 1>, k_inner<R, 2>})
             MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)IC::SMEM));
+        if constexpr (kW)
+            for (auto fn : {k_innerw<R, 1>, k_innerw<R, 2>})
+                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)IW::SMEM));
         if constexpr (kCpml) {
             for (auto fn : {k_cpml<RC, 1>, k_cpml<RC, 2>})
                 MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -541,13 +558,15 @@ private:
         if (zr.empty()) return w;
         w.empty = false;
         w.x_base = inner.lo[0] & ~3;
-        const int tiles_x = (inner.hi[0] - w.x_base + IC::TX - 1) / IC::TX;
-        const int tiles_y = (inner.hi[1] - inner.lo[1] + IC::TY - 1) / IC::TY;
+        const bool wk = mode == kInnerOnly && wide_;  // k_innerw: 64 x 24 tiles, 1 CTA/SM
+        const int ttx = wk ? IW::TX : IC::TX, tty = wk ? IW::TY : IC::TY;
+        const int tiles_x = (inner.hi[0] - w.x_base + ttx - 1) / ttx;
+        const int tiles_y = (inner.hi[1] - inner.lo[1] + tty - 1) / tty;
         std::vector<Item> tiles;
         for (const auto& r : zr)
             for (int ty = 0; ty < tiles_y; ++ty)
                 for (int tx = 0; tx < tiles_x; ++tx) tiles.push_back(Item{tx, ty, r.first, r.second});
-        finish_work(w, tiles, sms_ * inner_per_sm_, inner_zt_);
+        finish_work(w, tiles, sms_ * (wk ? 1 : inner_per_sm_), inner_zt_);
         return w;
     }
 
@@ -643,7 +662,17 @@ private:
         }
         const int bc = buf_index(p.pc), bp = buf_index(p.pp);
         const CUtensorMap &a = in_halo_[bc], &b = in_tile_[bp];
-        if (mode != kInnerOnly || col_inner_) {  // column kernel (MM_ZSLABS = 1, 2; R > 4)
+        if (mode == kInnerOnly && wide_) {
+            if constexpr (kW) {
+                const int g = std::min(w.ctas, inner_cap_);
+                if (order_ == 2)
+                    k_innerw<R, 2><<<g, IW::NT, IW::SMEM, s>>>(inw_halo_[bc], inw_tile_[bp],
+                                                                cv_inw_, ip);
+                else
+                    k_innerw<R, 1><<<g, IW::NT, IW::SMEM, s>>>(inw_halo_[bc], inw_tile_[bp],
+                                                                cv_inw_, ip);
+            }
+        } else if (mode != kInnerOnly || col_inner_) {  // column kernel (MM_ZSLABS = 1, 2; R > 4)
             if constexpr (kZs) {
                 constexpr size_t zsm = ZSlabCfg<R>::SMEM;
                 if (order_ == 2)
@@ -1129,6 +1158,7 @@ private:
     std::map<std::vector<int>, CpmlWork> cpml_cache_;
     double inner_zt_ = 48.0, bnd_zt_ = 48.0;
     int zmode_ = 0;
+    bool wide_ = false;  // R > 4: k_innerw serves the inner box
     bool pdl_ = true;
     bool overlap_ = false;
     cudaStream_t side_ = nullptr;
@@ -1138,6 +1168,7 @@ private:
     bool col_inner_ = false;
     const float* bufs_[3];
     CUtensorMap in_halo_[3], in_tile_[3], bd_halo_[3], bd_tile_[3], cv_in_, cv_bd_;
+    CUtensorMap inw_halo_[3], inw_tile_[3], cv_inw_;  // k_innerw (R > 4)
     BndMaps maps_;
     P1Maps p1maps_;
     DArr<float> dpz_[2];
