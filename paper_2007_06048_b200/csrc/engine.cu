@@ -45,7 +45,7 @@ const Tunable kTunables[] = {
     {"overlap", 1},      // interior kernel on a side stream beside the CPML kernels
     {"pdl", 1},          // programmatic dependent launch of k_bnd after k_p1
     {"epi_pdl", 0},      // (experiment) programmatic launch of the step epilogue behind the boundary kernel
-    {"inner_late", 0},   // (experiment) issue the interior kernel after pass 1 (1) or the boundary (2)
+    {"inner_late", 1},   // issue the interior kernel before pass 1 (0), after it (1) or after the boundary (2)
     {"main_prio", 0},    // (experiment) step stream at the greatest priority
     {"debug_sync", 0},   // (diagnostics) synchronize after every kernel (1) or every step (2)
     {"l2_promo", 2},     // TMA L2 promotion: 0 none, 1 64 B, 2 128 B, 3 256 B
@@ -53,6 +53,7 @@ const Tunable kTunables[] = {
     {"inner_ctas", 0},   // cap on the interior kernel's CTAs beside the CPML kernels (0: every slot)
     {"bnd_zt", 12},      // k_bnd planes per work item (target)
     {"p1_zt", 16},       // k_p1 planes per work item (target)
+    {"even_chunks", 0},  // work items: equal-length z chunks per tile (1) or zc-plane chunks (0)
     {"zslabs", -1},      // Z slabs: -1 auto, 0 k_bnd tiles, 1 k_zslab after k_inner, 2 k_zslab columns
     {"wide_inner", -1},  // r > 4 interior: -1 auto (2), 0 column kernel k_zslab, 1 unrolled k_inner, 2 k_innerw
     {"bnd_kinds", 7},    // (profiling) slab kinds k_bnd updates (bit mask X/Y/Z)

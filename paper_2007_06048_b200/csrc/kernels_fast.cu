@@ -173,11 +173,24 @@ void wave_items(const std::vector<Item>& tiles, int ctas, double target,
     const double per_cta = (double)tp / std::max(1, ctas);
     const int waves = std::max(1, (int)std::lround(per_cta / target));
     const int zc = std::max(4, (int)((tp + (long long)ctas * waves - 1) / ((long long)ctas * waves)));
-    for (int k = 0; (long long)k * zc < zmax; ++k)
+    if (tuning("even_chunks") == 0) {
+        for (int k = 0; (long long)k * zc < zmax; ++k)
+            for (const auto& t : tiles) {
+                const int zb = t.zlo + k * zc;
+                if (zb >= t.zhi) continue;
+                out.push_back(make_int4(t.tag, t.ty, zb, std::min(t.zhi, zb + zc)));
+            }
+        return;
+    }
+    // the same number of chunks per tile, of equal length (no short last
+    // chunk paying a whole z-window warm-up for a few planes)
+    const int kmax = (zmax + zc - 1) / zc;
+    for (int k = 0; k < kmax; ++k)
         for (const auto& t : tiles) {
-            const int zb = t.zlo + k * zc;
-            if (zb >= t.zhi) continue;
-            out.push_back(make_int4(t.tag, t.ty, zb, std::min(t.zhi, zb + zc)));
+            const int len = t.zhi - t.zlo, nc = (len + zc - 1) / zc;
+            if (k >= nc) continue;
+            out.push_back(make_int4(t.tag, t.ty, t.zlo + (int)((long long)len * k / nc),
+                                    t.zlo + (int)((long long)len * (k + 1) / nc)));
         }
 }
 
@@ -430,7 +443,12 @@ public:
         launch_pass1(p, 0, lay_.n[2], s);
         timer.end(t1, s);
         dbg(s, "pass1", p1_side_);
-        if (ov && inner_late_ == 1) fork_inner();  // (issue order only: still from the start)
+        // issued after pass 1 (default), the interior kernel still depends only
+        // on the step's start, but pass 1's launches reach the hardware first and
+        // take their SMs before the interior kernel fills the rest: issued first,
+        // the interior kernel won that race in most engines and left pass 1 (the
+        // critical path) the leftovers -- 159 instead of 145 us/step at 240^3
+        if (ov && inner_late_ == 1) fork_inner();
         const int t2 = timer.begin("boundary", s);
         if (fc)
             launch_boundary(p, 0, lay_.n[2], s, t2 < 0);  // (timer events break the PDL pair)
