@@ -36,6 +36,24 @@ using fast::smem_u32;
 __device__ __forceinline__ float fa(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float fs(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
+// lane pairs (FADD2 / FFMA2 with an opaque -0, fast_common.cuh): each lane
+// rounded like the scalar operation
+using fast::F2;
+using fast::f2;
+using fast::half2;
+using fast::unf2;
+// t + w * (a - b), both lanes (staggered_derivative_at's term)
+__device__ __forceinline__ F2 dterm2(F2 t, float w, F2 a, F2 b) {
+    return fast::acc2<2>(t, w, fast::fs2<2>(a, b));
+}
+// x + c * y lane-wise
+__device__ __forceinline__ F2 axpy2(F2 x, F2 c, F2 y) {
+    return fast::fa2<2>(x, fast::fmul2<2>(c, y));
+}
+__device__ __forceinline__ void unpack(const F2 (&v)[2], float (&d)[4]) {
+    unf2(v[0], d[0], d[1]);
+    unf2(v[1], d[2], d[3]);
+}
 
 template <int R>
 struct VdCfg {
@@ -345,33 +363,40 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, VdCfg<R>::MINB)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) xs[4 * h + e] = comp(v, e);
                 }
+                F2 t[2] = {fast::f2zero(), fast::f2zero()};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float t = 0.0f;
+                for (int m = 1; m <= R; ++m)
 #pragma unroll
-                    for (int m = 1; m <= R; ++m)
-                        t = fa(t, fm(P.w[0][m - 1], fs(xs[C::HX + e + m], xs[C::HX + e + 1 - m])));
-                    d[0][e] = t;
-                }
+                    for (int h = 0; h < 2; ++h)
+                        t[h] = dterm2(t[h], P.w[0][m - 1],
+                                      f2(xs[C::HX + 2 * h + m], xs[C::HX + 2 * h + 1 + m]),
+                                      f2(xs[C::HX + 2 * h + 1 - m], xs[C::HX + 2 * h + 2 - m]));
+                unpack(t, d[0]);
             }
             // y: rows y+m and y+1-m
+            {
+                F2 t[2] = {fast::f2zero(), fast::f2zero()};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) d[1][e] = d[2][e] = 0.0f;
+                for (int m = 1; m <= R; ++m) {
+                    const float4 u = lds4(Sc + m * C::BX), dn = lds4(Sc + (1 - m) * C::BX);
 #pragma unroll
-            for (int m = 1; m <= R; ++m) {
-                const float4 u = lds4(Sc + m * C::BX), dn = lds4(Sc + (1 - m) * C::BX);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    d[1][e] = fa(d[1][e], fm(P.w[1][m - 1], fs(comp(u, e), comp(dn, e))));
+                    for (int h = 0; h < 2; ++h)
+                        t[h] = dterm2(t[h], P.w[1][m - 1], half2(u, h), half2(dn, h));
+                }
+                unpack(t, d[1]);
             }
             // z: planes k+m <-> ring plane o+R-1+m, k+1-m <-> o+R-m
+            {
+                F2 t[2] = {fast::f2zero(), fast::f2zero()};
 #pragma unroll
-            for (int m = 1; m <= R; ++m) {
-                const float4 u = lds4(ring + ((o + R - 1 + m) % C::NSV) * C::PPLANE + soff);
-                const float4 dn = lds4(ring + ((o + R - m) % C::NSV) * C::PPLANE + soff);
+                for (int m = 1; m <= R; ++m) {
+                    const float4 u = lds4(ring + ((o + R - 1 + m) % C::NSV) * C::PPLANE + soff);
+                    const float4 dn = lds4(ring + ((o + R - m) % C::NSV) * C::PPLANE + soff);
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    d[2][e] = fa(d[2][e], fm(P.w[2][m - 1], fs(comp(u, e), comp(dn, e))));
+                    for (int h = 0; h < 2; ++h)
+                        t[h] = dterm2(t[h], P.w[2][m - 1], half2(u, h), half2(dn, h));
+                }
+                unpack(t, d[2]);
             }
             const int st = qn % C::NQV;
             fast::mbar_wait(barQ + 8 * st, (phQ >> st) & 1u);
@@ -387,7 +412,9 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, VdCfg<R>::MINB)
                     const float4 v = lds4(Q + (a + 1) * C::TILE);
                     float out[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) out[e] = fa(comp(v, e), fm(comp(ir, e), d[a][e]));
+                    for (int h = 0; h < 2; ++h)
+                        unf2(axpy2(half2(v, h), half2(ir, h), f2(d[a][2 * h], d[a][2 * h + 1])),
+                             out[2 * h], out[2 * h + 1]);
                     st4v(P.v[a] + oo, out, S);
                 }
             }
@@ -498,34 +525,41 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, VdCfg<R>::MINB)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) xs[4 * h + e] = comp(v, e);
                 }
+                F2 t[2] = {fast::f2zero(), fast::f2zero()};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float t = 0.0f;
+                for (int m = 1; m <= R; ++m)
 #pragma unroll
-                    for (int m = 1; m <= R; ++m)
-                        t = fa(t, fm(P.w[0][m - 1], fs(xs[C::HX + e + m - 1], xs[C::HX + e - m])));
-                    d[0][e] = t;
-                }
+                    for (int h = 0; h < 2; ++h)
+                        t[h] = dterm2(t[h], P.w[0][m - 1],
+                                      f2(xs[C::HX + 2 * h + m - 1], xs[C::HX + 2 * h + m]),
+                                      f2(xs[C::HX + 2 * h - m], xs[C::HX + 2 * h + 1 - m]));
+                unpack(t, d[0]);
             }
             // y: rows y+m-1 and y-m
+            {
+                F2 t[2] = {fast::f2zero(), fast::f2zero()};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) d[1][e] = d[2][e] = 0.0f;
+                for (int m = 1; m <= R; ++m) {
+                    const float4 u = lds4(Q + C::VXB + yoff + (m - 1) * C::TX);
+                    const float4 dn = lds4(Q + C::VXB + yoff - m * C::TX);
 #pragma unroll
-            for (int m = 1; m <= R; ++m) {
-                const float4 u = lds4(Q + C::VXB + yoff + (m - 1) * C::TX);
-                const float4 dn = lds4(Q + C::VXB + yoff - m * C::TX);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    d[1][e] = fa(d[1][e], fm(P.w[1][m - 1], fs(comp(u, e), comp(dn, e))));
+                    for (int h = 0; h < 2; ++h)
+                        t[h] = dterm2(t[h], P.w[1][m - 1], half2(u, h), half2(dn, h));
+                }
+                unpack(t, d[1]);
             }
             // z: planes k+m-1 <-> ring plane o+R+m-1, k-m <-> o+R-m
+            {
+                F2 t[2] = {fast::f2zero(), fast::f2zero()};
 #pragma unroll
-            for (int m = 1; m <= R; ++m) {
-                const float4 u = lds4(ring + ((o + R + m - 1) % C::NSP) * C::TILE + toff);
-                const float4 dn = lds4(ring + ((o + R - m) % C::NSP) * C::TILE + toff);
+                for (int m = 1; m <= R; ++m) {
+                    const float4 u = lds4(ring + ((o + R + m - 1) % C::NSP) * C::TILE + toff);
+                    const float4 dn = lds4(ring + ((o + R - m) % C::NSP) * C::TILE + toff);
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    d[2][e] = fa(d[2][e], fm(P.w[2][m - 1], fs(comp(u, e), comp(dn, e))));
+                    for (int h = 0; h < 2; ++h)
+                        t[h] = dterm2(t[h], P.w[2][m - 1], half2(u, h), half2(dn, h));
+                }
+                unpack(t, d[2]);
             }
             if (S.any) {
                 psi_apply(d, ps, P, S, o, k);
@@ -533,8 +567,12 @@ __global__ void __launch_bounds__(VdCfg<R>::NT, VdCfg<R>::MINB)
                 const float4 pc = lds4(Q + C::VXB + C::VYB + C::TILE + toff);
                 float out[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    out[e] = fa(comp(pc, e), fm(comp(dt, e), fa(fa(d[0][e], d[1][e]), d[2][e])));
+                for (int h = 0; h < 2; ++h) {
+                    const F2 sum = fast::fa2<2>(
+                        fast::fa2<2>(f2(d[0][2 * h], d[0][2 * h + 1]), f2(d[1][2 * h], d[1][2 * h + 1])),
+                        f2(d[2][2 * h], d[2][2 * h + 1]));
+                    unf2(axpy2(half2(pc, h), half2(dt, h), sum), out[2 * h], out[2 * h + 1]);
+                }
                 st4v(P.p + o0 + (long long)o * L.plane, out, S);
             }
             __syncthreads();  // vz plane o and stage o are free
