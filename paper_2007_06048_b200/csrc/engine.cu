@@ -43,10 +43,13 @@ const Tunable kTunables[] = {
     {"cpml_fused", 0},   // fast mode: one-pass CPML kernel k_cpml where the layout allows it (0: k_p1 + k_bnd)
     {"cpml_zt", 0},      // k_cpml planes per work item (0: automatic)
     {"overlap", 1},      // interior kernel on a side stream beside the CPML kernels
-    {"pdl", 1},          // programmatic dependent launch of k_bnd after k_p1
+    {"pdl", -1},         // programmatic launch of k_bnd after k_p1: -1 auto (grids < 6 M points), 0 off, 1 on
+                         // (on big grids its early CTAs race the interior kernel for SMs while
+                         // pass 1 drains: 145-158 us/step at 240^3 by engine, 145 without)
     {"epi_pdl", 0},      // (experiment) programmatic launch of the step epilogue behind the boundary kernel
     {"inner_late", 1},   // issue the interior kernel before pass 1 (0), after it (1) or after the boundary (2)
-    {"main_prio", 0},    // (experiment) step stream at the greatest priority
+    {"main_prio", 2},    // pass 1 -> boundary streams above the interior kernel's: 0 none, 1 the step's
+                         // stream, 2 both pass-1 streams (the CPML chain wins every race for SMs)
     {"debug_sync", 0},   // (diagnostics) synchronize after every kernel (1) or every step (2)
     {"l2_promo", 2},     // TMA L2 promotion: 0 none, 1 64 B, 2 128 B, 3 256 B
     {"inner_zt", 48},    // k_inner planes per work item (target)
@@ -334,8 +337,8 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     auto e = std::make_unique<mm_cd_engine>();
     e->device = device;
     e->mode = mode;
-    // tuning "main_prio" (experiment): the step's stream at the greatest
-    // priority, above the interior kernel's side stream
+    // tuning "main_prio": the step's stream (pass 1 -> boundary, the critical
+    // path) at the greatest priority, above the interior kernel's side stream
     if (tuning("main_prio") > 0) {
         int lo = 0, hi = 0;
         MM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));

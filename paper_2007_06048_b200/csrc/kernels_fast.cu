@@ -254,13 +254,18 @@ public:
         bnd_kinds_ = (int)tuning("bnd_kinds");
         bnd_cap_ = tuning("bnd_ctas") > 0 ? (int)tuning("bnd_ctas") : 1 << 30;
         p1_axes_ = (int)tuning("p1_axes");
-        // side streams at the lowest priority: pass 1's z runs (on the step's
-        // stream, the critical path) are scheduled first
+        // pass 1's x/y runs at the step stream's priority (tuning main_prio 2),
+        // above the interior kernel's side stream (lowest): when both have CTAs
+        // pending, the CPML chain's go first (without priorities the interior
+        // kernel won that race in some engines: 145-159 us/step at 240^3)
         int prio_lo = 0, prio_hi = 0;
         MM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         MM_CUDA(cudaStreamCreateWithPriority(&p1_side_, cudaStreamNonBlocking,
                                              tuning("main_prio") >= 2 ? prio_hi : prio_lo));
-        pdl_ = tuning("pdl") != 0;
+        {  // auto: on for grids whose steps replay as CUDA graphs (step_graph)
+            const long long pd = tuning("pdl");
+            pdl_ = pd < 0 ? (double)lay.n[0] * lay.n[1] * lay.n[2] < 6.0e6 : pd != 0;
+        }
         MM_CUDA(cudaEventCreateWithFlags(&p1_fork_, cudaEventDisableTiming));
         MM_CUDA(cudaEventCreateWithFlags(&p1_join_, cudaEventDisableTiming));
         if (overlap_) {
