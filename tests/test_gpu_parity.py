@@ -262,6 +262,32 @@ def test_fast_equals_strict_large_random_state(mm):
     assert np.array_equal(a, b), f"{int(np.count_nonzero(a != b))} points differ"
 
 
+@pytest.mark.parametrize("radius,n,nd", [
+    (8, (200, 150, 170), (20, 17, 23)),   # k_innerw: 64 x 24 tiles, partial in x and y
+    (8, (131, 260, 90), (9, 30, 12)),     # many y tiles, short z columns
+])
+def test_fast_equals_strict_wide_stencil_random_state(mm, radius, n, nd):
+    """The r > 4 interior kernel (register z window shifted every 4 planes,
+    x/y from the centre plane) over many work items and partial tiles, random
+    p_prev / p_cur everywhere: fast == strict bit for bit."""
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0), radius)
+    model = mm.random_model(grid, seed=3)
+    rng = np.random.default_rng(8)
+    p0 = rng.standard_normal(grid.shape, dtype=np.float32)
+    p1 = rng.standard_normal(grid.shape, dtype=np.float32)
+    opts = mm.EngineOptions(ndamping=nd, taper=True)
+    out = {}
+    for md in ("fast", "strict"):
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, 1.0e-3, model.vmax, mode=md)
+        e.set_state(p0, p1)
+        for s in range(5):
+            e.step(0.25, (n[0] // 2, n[1] // 3, n[2] // 2))
+        out[md] = (e.pressure(), e.pressure_prev())
+        del e
+    for a, b in zip(out["fast"], out["strict"]):
+        assert np.array_equal(a, b), f"{int(np.count_nonzero(a != b))} points differ"
+
+
 def test_two_engine_zslab_halo_exchange_bitwise(mm):
     """Two z-slab engines on one device, halos moved through the C-ABI plane
     pointers, equal the single engine (test_dist.cpp:107-118 restated)."""
