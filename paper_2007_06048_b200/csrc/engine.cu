@@ -56,7 +56,8 @@ const Tunable kTunables[] = {
     {"inner_ctas", 0},   // cap on the interior kernel's CTAs beside the CPML kernels (0: every slot)
     {"bnd_zt", 12},      // k_bnd planes per work item (target)
     {"p1_zt", 16},       // k_p1 planes per work item (target)
-    {"even_chunks", 0},  // work items: equal-length z chunks per tile (1) or zc-plane chunks (0)
+    {"even_chunks", 5},  // equal-length z chunks per tile (bit mask: 1 interior, 2 boundary, 4 pass-1 x/y;
+                         // 240^3: 143.6 with 5, 145.0 with 0, boundary chunks 146.5)
     {"zslabs", -1},      // Z slabs: -1 auto, 0 k_bnd tiles, 1 k_zslab after k_inner, 2 k_zslab columns
     {"wide_inner", -1},  // r > 4 interior: -1 auto (2), 0 column kernel k_zslab, 1 unrolled k_inner, 2 k_innerw
     {"bnd_kinds", 7},    // (profiling) slab kinds k_bnd updates (bit mask X/Y/Z)

@@ -161,7 +161,7 @@ struct Item {
     int tag, ty, zlo, zhi;
 };
 void wave_items(const std::vector<Item>& tiles, int ctas, double target,
-                std::vector<int4>& out) {
+                std::vector<int4>& out, bool even = false) {
     out.clear();
     if (tiles.empty()) return;
     long long tp = 0;
@@ -173,7 +173,7 @@ void wave_items(const std::vector<Item>& tiles, int ctas, double target,
     const double per_cta = (double)tp / std::max(1, ctas);
     const int waves = std::max(1, (int)std::lround(per_cta / target));
     const int zc = std::max(4, (int)((tp + (long long)ctas * waves - 1) / ((long long)ctas * waves)));
-    if (tuning("even_chunks") == 0) {
+    if (!even) {
         for (int k = 0; (long long)k * zc < zmax; ++k)
             for (const auto& t : tiles) {
                 const int zb = t.zlo + k * zc;
@@ -544,9 +544,10 @@ private:
         return k;
     }
 
-    void finish_work(Work& w, const std::vector<Item>& tiles, int ctas, double target) {
+    void finish_work(Work& w, const std::vector<Item>& tiles, int ctas, double target,
+                     bool even = false) {
         std::vector<int4> items;
-        wave_items(tiles, ctas, target, items);
+        wave_items(tiles, ctas, target, items, even);
         w.nitems = (int)items.size();
         w.ctas = std::max(1, std::min(ctas, w.nitems));
         w.segs.set(items, stream_setup_);
@@ -589,7 +590,8 @@ private:
         for (const auto& r : zr)
             for (int ty = 0; ty < tiles_y; ++ty)
                 for (int tx = 0; tx < tiles_x; ++tx) tiles.push_back(Item{tx, ty, r.first, r.second});
-        finish_work(w, tiles, sms_ * (wk ? 1 : inner_per_sm_), inner_zt_);
+        finish_work(w, tiles, sms_ * (wk ? 1 : inner_per_sm_), inner_zt_,
+                    (tuning("even_chunks") & 1) != 0);
         return w;
     }
 
@@ -632,7 +634,7 @@ private:
         }
         if (items.empty()) return w;
         w.empty = false;
-        finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_);
+        finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_, (tuning("even_chunks") & 2) != 0);
         return w;
     }
 
@@ -873,7 +875,7 @@ private:
                     }
                 // two launches: the x/y runs (many small CTAs) and the z runs
                 std::vector<int4> items;
-                wave_items(tiles, sms_ * p1x_per_sm_, p1_zt_, items);
+                wave_items(tiles, sms_ * p1x_per_sm_, p1_zt_, items, (tuning("even_chunks") & 4) != 0);
                 e.nx = (int)items.size();
                 e.ctas_x = std::max(1, std::min(sms_ * p1x_per_sm_, e.nx));
                 e.nz = (int)zitems.size();
