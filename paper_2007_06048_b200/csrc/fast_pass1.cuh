@@ -94,6 +94,13 @@ struct P1Tile {
     }
 };
 
+// Producer lanes: 1 = lane 0 streams items, the p_cur ring and the psi stages
+// (a stage issued as the ring reaches it); 2 = lane 1 streams the psi stages.
+#ifndef MM_P1_LANES
+#define MM_P1_LANES 2
+#endif
+constexpr bool kSplitLanes = MM_P1_LANES == 2;
+
 template <int R, int ORD, bool Z>
 __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
     k_p1(const __grid_constant__ P1Maps M, const P1Params P) {
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(fullI + 8 * s, 1);
-            mbar_init(emptyI + 8 * s, C::NCW);
+            mbar_init(emptyI + 8 * s, C::NCW + (kSplitLanes ? 1 : 0));  // + the stage lane
         }
         fence_barrier_init();
     }
@@ -173,14 +180,45 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                     mbar_expect_tx(bar, pbytes);
                     tma_load_3d(smem_u32(ring + s * C::PSLOT), pmap, px, py, z + L.r, bar);
                     ++np;
-                    for (; oq < T.nout && oq <= j - 2 * T.w + C::QLEAD; ++oq) issue_q(oq);
+                    if (!kSplitLanes)
+                        for (; oq < T.nout && oq <= j - 2 * T.w + C::QLEAD; ++oq) issue_q(oq);
                 }
-                for (; oq < T.nout; ++oq) issue_q(oq);
+                if (!kSplitLanes)
+                    for (; oq < T.nout; ++oq) issue_q(oq);
             }
             __threadfence();
             if (atomicAdd(P.wq.ctr + 1, 1) == (int)gridDim.x - 1) {
                 atomicExch(P.wq.ctr, 0);
                 atomicExch(P.wq.ctr + 1, 0);
+            }
+        } else if (kSplitLanes && lane == 1) {
+            // the psi stages, as far ahead as the stage ring allows (not gated
+            // by the p_cur ring's progress)
+            unsigned nq = 0, ni = 0;
+            for (;;) {
+                int4 sg;
+                {
+                    const int s = ni & 1;
+                    mbar_wait(fullI + 8 * s, (ni >> 1) & 1);
+                    sg = items[s];
+                    mbar_arrive_b(emptyI + 8 * s);
+                    ++ni;
+                }
+                if (sg.w < 0) break;
+                const P1Tile<R, Z> T(P, sg);
+                const CpmlRun& run = P.run[T.ax][T.side];
+                const int qx = T.x0 - (T.ax == 0 ? run.org : 0);
+                const int qy = T.y0 - (T.ax == 1 ? run.org : 0);
+                const int qz = T.ax == 2 ? run.org : 0;
+                for (int o = 0; o < T.nout; ++o) {
+                    const int s = nq % C::NQ;
+                    mbar_wait_sleep(emptyQ + 8 * s, ((nq / C::NQ) & 1) ^ 1);
+                    const uint32_t bar = fullQ + 8 * s;
+                    mbar_expect_tx(bar, 4u * C::PSI_N);
+                    tma_load_3d(smem_u32(qring + s * C::PSI), &M.psi[T.ax][T.side], qx, qy,
+                                T.zb + o - qz, bar);
+                    ++nq;
+                }
             }
         }
         return;
