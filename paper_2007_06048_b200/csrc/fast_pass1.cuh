@@ -30,10 +30,19 @@ namespace fast {
 #define MM_P1Z_TY 16
 #endif
 
+// z runs: x points per consumer thread.  2 (twice the warps per tile, half the
+// serial work per warp and plane) measured slower: z items alone 27.7 vs 25.1
+// us at 240^3, 66 vs 58 at 512^3 -- the items' chains are not bound by the
+// work of one warp.
+#ifndef MM_P1Z_PX
+#define MM_P1Z_PX 4
+#endif
+
 template <int R, bool Z>
 struct P1Cfg {
     static constexpr int TX = 32, TY = Z ? MM_P1Z_TY : 16;
-    static constexpr int NC = (TX / 4) * TY;  // 128 consumer threads, float4 each
+    static constexpr int PX = Z ? MM_P1Z_PX : 4;  // x points per consumer thread
+    static constexpr int NC = (TX / PX) * TY;  // consumer threads
     static constexpr int NCW = NC / 32;
     static constexpr int NT = NC + 32;        // + producer warp
     static constexpr int HX = R <= 4 ? 4 : 8;  // x halo (16-byte aligned TMA starts)
@@ -225,7 +234,7 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
     }
 
     // ---------------------------------------------------------------- consumers
-    const int tx = tid % (C::TX / 4), ty = tid / (C::TX / 4);
+    const int tx = tid % (C::TX / C::PX), ty = tid / (C::TX / C::PX);
     unsigned np = 0, nq = 0, ni = 0;
     for (;;) {
         int4 sg;
@@ -242,21 +251,23 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
         const int ax = T.ax;
         const RunDesc& d = P.rd[sg.x & 7];
         const CpmlRun& run = P.run[ax][T.side];
-        const int x = T.x0 + 4 * tx, y = T.y0 + ty;
-        bool ok[4];
+        const int x = T.x0 + C::PX * tx, y = T.y0 + ty;
+        bool ok[C::PX];
+        bool all = true, any = false;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
+        for (int e = 0; e < C::PX; ++e) {
             ok[e] = x + e >= d.lo[0] && x + e < d.hi[0] && y >= d.lo[1] && y < d.hi[1];
-        const bool all = ok[0] && ok[1] && ok[2] && ok[3];
-        const bool any = ok[0] || ok[1] || ok[2] || ok[3];
+            all = all && ok[e];
+            any = any || ok[e];
+        }
         float c1[R];
 #pragma unroll
         for (int m = 0; m < R; ++m) c1[m] = P.c1[ax][m];
         // damping coefficients: per x (x runs), per y (y runs), per z (z runs)
-        float av[4], bv[4];
+        float av[C::PX], bv[C::PX];
         if (ax == 0) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
+            for (int e = 0; e < C::PX; ++e) {
                 const int xc = min(max(x + e, 0), L.n[0] - 1);
                 av[e] = __ldg(P.ta[0] + xc);
                 bv[e] = __ldg(P.tb[0] + xc);
@@ -266,7 +277,7 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
             const float a = ax == 1 ? __ldg(P.ta[1] + yc) : 0.f;
             const float b = ax == 1 ? __ldg(P.tb[1] + yc) : 0.f;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
+            for (int e = 0; e < C::PX; ++e) {
                 av[e] = a;
                 bv[e] = b;
             }
@@ -274,39 +285,57 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
         float* dst = run.psi + run_off(run, ax, x, y, T.zb);
         const long long zstep = run.s2;
         // offset of this thread's 4 points in a p slot
-        const int poff = ax == 0 ? ty * C::BXX + C::HX + 4 * tx
-                         : ax == 1 ? (ty + R) * C::TX + 4 * tx
-                                   : ty * C::TX + 4 * tx;
-        const int qoff = ty * C::TX + 4 * tx;
-        auto store4 = [&](float* q, const float4& v) {
-            if (all) {
-                *reinterpret_cast<float4*>(q) = v;
-            } else if (any) {
-                if (ok[0]) q[0] = v.x;
-                if (ok[1]) q[1] = v.y;
-                if (ok[2]) q[2] = v.z;
-                if (ok[3]) q[3] = v.w;
-            }
-        };
+        const int poff = ax == 0 ? ty * C::BXX + C::HX + C::PX * tx
+                         : ax == 1 ? (ty + R) * C::TX + C::PX * tx
+                                   : ty * C::TX + C::PX * tx;
+        const int qoff = ty * C::TX + C::PX * tx;
         if constexpr (Z) {
             // z runs (an item covers the whole run, zb = lo, ze = hi).  The
             // new psi_z of this thread's points rides a register queue
             // zq[k] = plane o-1-2R+k (zeros outside the run), from which dpsi_z
             // at plane o-1-R is emitted while plane o is computed; the
             // p_cur z window is addressed through rotating slot offsets.
-            float4 zq[2 * R + 1];
+            constexpr int NPR = C::PX / 2;  // lane pairs per thread
+            F2 zq[2 * R + 1][NPR];
 #pragma unroll
-            for (int k = 0; k <= 2 * R; ++k) zq[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k <= 2 * R; ++k)
+#pragma unroll
+                for (int h = 0; h < NPR; ++h) zq[k][h] = f2zero();
+            // PX points from / to shared or global memory as lane pairs
+            auto ldp = [](const float* q, F2 (&v)[NPR]) {
+#pragma unroll
+                for (int h = 0; h < NPR; ++h) v[h].r = reinterpret_cast<const unsigned long long*>(q)[h];
+            };
+            auto stp = [&](float* q, const F2 (&v)[NPR]) {
+                if (all) {
+                    if constexpr (NPR == 2) {
+                        *reinterpret_cast<float4*>(q) = f4(v[0], v[1]);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < NPR; ++h)
+                            reinterpret_cast<unsigned long long*>(q)[h] = v[h].r;
+                    }
+                } else if (any) {
+#pragma unroll
+                    for (int h = 0; h < NPR; ++h) {
+                        float a0, a1;
+                        unf2(v[h], a0, a1);
+                        if (ok[2 * h]) q[2 * h] = a0;
+                        if (ok[2 * h + 1]) q[2 * h + 1] = a1;
+                    }
+                }
+            };
             float* dz_p = P.dpz[T.side] + x + (long long)y * run.s1;  // plane od = -R
             auto emit_dpz = [&]() {  // dpsi_z at queue centre (plane od)
-                F2 dz[2] = {f2zero(), f2zero()};  // lane pairs (x, x+1), (x+2, x+3)
+                F2 dz[NPR];
+#pragma unroll
+                for (int h = 0; h < NPR; ++h) dz[h] = f2zero();  // lane pairs (x, x+1), ...
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        dz[h] = d1_term2<ORD>(dz[h], c1[m - 1], half2(zq[R + m], h),
-                                              half2(zq[R - m], h));
-                store4(dz_p, f4(dz[0], dz[1]));
+                    for (int h = 0; h < NPR; ++h)
+                        dz[h] = d1_term2<ORD>(dz[h], c1[m - 1], zq[R + m][h], zq[R - m][h]);
+                stp(dz_p, dz);
                 dz_p += run.s2;
             };
             int wo[2 * R + 1];     // p_cur slot offsets of planes j-2R .. j
@@ -326,17 +355,22 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                     // it is independent of this plane's psi (more ILP per plane)
                     if (o > 0) emit_dpz();
                     const float az = __ldg(P.ta[2] + z), bz = __ldg(P.tb[2] + z);
-                    F2 dp[2] = {f2zero(), f2zero()};
+                    F2 dp[NPR];
+#pragma unroll
+                    for (int h = 0; h < NPR; ++h) dp[h] = f2zero();
 #pragma unroll
                     for (int m = 1; m <= R; ++m) {
-                        const float4 u4 = lds4(ring + wo[R + m]), d4 = lds4(ring + wo[R - m]);
+                        F2 u[NPR], dn[NPR];
+                        ldp(ring + wo[R + m], u);
+                        ldp(ring + wo[R - m], dn);
 #pragma unroll
-                        for (int h = 0; h < 2; ++h)
-                            dp[h] = d1_term2<ORD>(dp[h], c1[m - 1], half2(u4, h), half2(d4, h));
+                        for (int h = 0; h < NPR; ++h)
+                            dp[h] = d1_term2<ORD>(dp[h], c1[m - 1], u[h], dn[h]);
                     }
                     const int st = nq % C::NQ;
                     mbar_wait(fullQ + 8 * st, (nq / C::NQ) & 1);
-                    float4 v = lds4(qring + st * C::PSI + qoff);
+                    F2 v[NPR];
+                    ldp(qring + st * C::PSI + qoff, v);
                     __syncwarp();
                     if (lane == 0) {
                         mbar_arrive_b(emptyQ + 8 * st);
@@ -345,12 +379,15 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                     ++nq;
                     if (++rel == C::NS) rel = 0;
                     // reference: psi = b * psi + a * dp  (propagator_impl.hpp:118-120)
-                    v = f4(acc2<ORD>(fm2<ORD>(az, dp[0]), bz, half2(v, 0)),
-                           acc2<ORD>(fm2<ORD>(az, dp[1]), bz, half2(v, 1)));
-                    store4(dst + (long long)o * zstep, v);
 #pragma unroll
-                    for (int k = 0; k < 2 * R; ++k) zq[k] = zq[k + 1];
-                    zq[2 * R] = v;
+                    for (int h = 0; h < NPR; ++h) v[h] = acc2<ORD>(fm2<ORD>(az, dp[h]), bz, v[h]);
+                    stp(dst + (long long)o * zstep, v);
+#pragma unroll
+                    for (int k = 0; k < 2 * R; ++k)
+#pragma unroll
+                        for (int h = 0; h < NPR; ++h) zq[k][h] = zq[k + 1][h];
+#pragma unroll
+                    for (int h = 0; h < NPR; ++h) zq[2 * R][h] = v[h];
                 }
                 ++np;
                 if (++sl == C::NS) sl = 0, ph ^= 1;
@@ -361,8 +398,11 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
 #pragma unroll 1
             for (int t = 0; t < 2 * R; ++t) {
 #pragma unroll
-                for (int k = 0; k < 2 * R; ++k) zq[k] = zq[k + 1];
-                zq[2 * R] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int k = 0; k < 2 * R; ++k)
+#pragma unroll
+                    for (int h = 0; h < NPR; ++h) zq[k][h] = zq[k + 1][h];
+#pragma unroll
+                for (int h = 0; h < NPR; ++h) zq[2 * R][h] = f2zero();
                 emit_dpz();
             }
 #pragma unroll 1
@@ -372,6 +412,16 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
                 if (++rel == C::NS) rel = 0;
             }
         } else {
+        auto store4 = [&](float* q, const float4& v) {
+            if (all) {
+                *reinterpret_cast<float4*>(q) = v;
+            } else if (any) {
+                if (ok[0]) q[0] = v.x;
+                if (ok[1]) q[1] = v.y;
+                if (ok[2]) q[2] = v.z;
+                if (ok[3]) q[3] = v.w;
+            }
+        };
 #pragma unroll 1
         for (int j = 0; j < T.nring; ++j) {
             const int s = np % C::NS;
