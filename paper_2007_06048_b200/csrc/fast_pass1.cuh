@@ -29,6 +29,9 @@ namespace fast {
 #ifndef MM_P1Z_TY
 #define MM_P1Z_TY 16
 #endif
+#ifndef MM_P1X_TY
+#define MM_P1X_TY 16
+#endif
 
 // z runs: x points per consumer thread.  2 (twice the warps per tile, half the
 // serial work per warp and plane) measured slower: z items alone 27.7 vs 25.1
@@ -40,7 +43,7 @@ namespace fast {
 
 template <int R, bool Z>
 struct P1Cfg {
-    static constexpr int TX = 32, TY = Z ? MM_P1Z_TY : 16;
+    static constexpr int TX = 32, TY = Z ? MM_P1Z_TY : MM_P1X_TY;
     static constexpr int PX = Z ? MM_P1Z_PX : 4;  // x points per consumer thread
     static constexpr int NC = (TX / PX) * TY;  // consumer threads
     static constexpr int NCW = NC / 32;
