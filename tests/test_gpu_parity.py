@@ -288,6 +288,40 @@ def test_fast_equals_strict_wide_stencil_random_state(mm, radius, n, nd):
         assert np.array_equal(a, b), f"{int(np.count_nonzero(a != b))} points differ"
 
 
+@pytest.mark.parametrize("knobs", [
+    dict(main_prio=0, inner_late=0, pdl=1, even_chunks=0),   # round-1 schedule
+    dict(pdl=1, epi_pdl=1),           # programmatic boundary + epilogue launches
+    dict(step_graph=1, pdl=1),        # graph-replayed steps with the PDL pair
+    dict(overlap=0, even_chunks=7),   # serial kernels, equal-length chunks everywhere
+])
+def test_step_schedule_variants_bitwise(mm, knobs):
+    """The schedule knobs (stream priorities, issue order, programmatic
+    launches, graphs, work-item chunking) change when kernels run, never what
+    they compute: every variant equals the default schedule bit for bit,
+    host-driven steps and the device loop."""
+    n, nd, steps = (96, 88, 104), (27, 27, 27), 30
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0))
+    model = mm.random_model(grid, seed=2)
+    opts = mm.EngineOptions(ndamping=nd, taper=True)
+    w = mm.ricker(25.0, 1.0e-3, steps).samples
+    src = (48, 40, 50)
+
+    def run():
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, 1.0e-3, model.vmax)
+        e.run(w[:20], src, record=False)
+        for s in range(20, steps):
+            e.step(float(w[s]), src)
+        out = (e.pressure(), e.pressure_prev())
+        del e
+        return out
+
+    want = run()
+    with tuned(**knobs):
+        got = run()
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b), f"{int(np.count_nonzero(a != b))} points differ"
+
+
 def test_two_engine_zslab_halo_exchange_bitwise(mm):
     """Two z-slab engines on one device, halos moved through the C-ABI plane
     pointers, equal the single engine (test_dist.cpp:107-118 restated)."""
