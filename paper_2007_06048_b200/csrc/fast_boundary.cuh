@@ -58,7 +58,10 @@ struct BndCfg {
     static constexpr int NBAR = 2 * NS + 2 * NQD + 4;
     // bytes per CTA: two CTAs per SM up to R = 4; one (with the registers of
     // two) for wider stencils, whose z window needs a deeper ring
-    static constexpr int CTAS = R <= 4 ? 2 : 1;
+#ifndef MM_BND_CTAS4
+#define MM_BND_CTAS4 2
+#endif
+    static constexpr int CTAS = R <= 4 ? MM_BND_CTAS4 : 1;
     static constexpr int BUDGET = CTAS == 2 ? 112 * 1024 : 220 * 1024;
     static constexpr int MAXREG = CTAS == 2 ? 128 : 255;
     static constexpr int QB_RAW = (BUDGET - 4 * NS * PPLANE - 8 * NBAR - 4 * NQD - 64) / 4;
