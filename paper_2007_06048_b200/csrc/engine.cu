@@ -56,6 +56,8 @@ const Tunable kTunables[] = {
     {"inner_ctas", 0},   // cap on the interior kernel's CTAs beside the CPML kernels (0: every slot)
     {"bnd_zt", 12},      // k_bnd planes per work item (target)
     {"p1_zt", 16},       // k_p1 planes per work item (target)
+    {"field_stagger", 1024},  // pressure / c field k starts k x this many floats into its allocation
+                            // (240^3: the fast step mode in 6 of 7 engines vs 2-3 of 7 unstaggered)
     {"even_chunks", 5},  // equal-length z chunks per tile (bit mask: 1 interior, 2 boundary, 4 pass-1 x/y;
                          // 240^3: 143.6 with 5, 145.0 with 0, boundary chunks 146.5)
     {"zslabs", -1},      // Z slabs: -1 auto, 0 k_bnd tiles, 1 k_zslab after k_inner, 2 k_zslab columns
@@ -386,9 +388,16 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
     }
     // device fields
     const Layout& L = e->lay;
-    for (int b = 0; b < 3; ++b) e->p[b].alloc_zero(L.total, e->stream);
-    e->vp.alloc_zero(L.total, e->stream);
-    e->cv.alloc_zero(L.total, e->stream);
+    // tuning field_stagger: field k starts k x stagger floats into its
+    // allocation (multiples of 32: rows stay 128-byte aligned), so the same
+    // point of p_prev, p_cur, p_next and c -- streamed side by side by every
+    // kernel -- does not sit at the same offset of identically aligned
+    // allocations (the step was 141 or 144.5 us at 240^3 by engine: unstaggered
+    // 2-3 of 7 engines fast, staggered by 1024 floats 6 of 7)
+    const size_t stag = (size_t)std::max(0LL, tuning("field_stagger")) / 32 * 32;
+    for (int b = 0; b < 3; ++b) e->p[b].alloc_zero(L.total, e->stream, stag * (size_t)b);
+    e->vp.alloc_zero(L.total, e->stream, stag * 3);
+    e->cv.alloc_zero(L.total, e->stream, stag * 4);
     e->from_host(vp.data(), e->vp.ptr);
     launch_velocity_coeff(e->vp.ptr, e->cv.ptr, e->dt2, L.total, e->stream);
     e->setup_cpml();

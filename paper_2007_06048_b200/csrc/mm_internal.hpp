@@ -106,24 +106,26 @@ void validate_vp(const float* vp, const HostGrid& g, float* vmin, float* vmax);
 template <typename T>
 struct DevBuf {
     T* ptr = nullptr;
+    T* base = nullptr;  // the allocation (ptr = base + a stagger of `pad` elements)
     size_t count = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { reset(); }
     void reset() {
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
+        if (base) cudaFree(base);
+        ptr = base = nullptr;
         count = 0;
     }
-    void alloc(size_t n) {
+    void alloc(size_t n, size_t pad = 0) {
         reset();
         if (n == 0) return;
-        MM_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+        MM_CUDA(cudaMalloc(&base, (n + pad) * sizeof(T)));
+        ptr = base + pad;
         count = n;
     }
-    void alloc_zero(size_t n, cudaStream_t s) {
-        alloc(n);
+    void alloc_zero(size_t n, cudaStream_t s, size_t pad = 0) {
+        alloc(n, pad);
         if (n) MM_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));
     }
     void upload(const T* host, size_t n, cudaStream_t s) {
