@@ -37,7 +37,10 @@ struct BndCfg {
     static constexpr int TXT = 8;        // threads per row
     static constexpr int TX = PX * TXT;  // 32
     // 7 consumer warps x 4 rows: 28 rows also tile the 27-row Y slabs.
-    static constexpr int TY = 28;
+#ifndef MM_BND_TY
+#define MM_BND_TY 28
+#endif
+    static constexpr int TY = MM_BND_TY;
     static constexpr int NC = TXT * TY;  // 224 consumer threads
     static constexpr int NCW = NC / 32;
     static constexpr int NT = NC + 32;   // + producer warp
@@ -63,7 +66,7 @@ struct BndCfg {
 #endif
     static constexpr int CTAS = R <= 4 ? MM_BND_CTAS4 : 1;
     static constexpr int BUDGET = CTAS == 2 ? 112 * 1024 : 220 * 1024;
-    static constexpr int MAXREG = CTAS == 2 ? 128 : 255;
+    static constexpr int MAXREG = CTAS == 2 ? 65536 / (2 * NT) / 8 * 8 : 255;
     static constexpr int QB_RAW = (BUDGET - 4 * NS * PPLANE - 8 * NBAR - 4 * NQD - 64) / 4;
     static constexpr int QMAX = 7 * TILE + PSX + 2 * PSY;
     static constexpr int QB = QB_RAW > QMAX ? QB_RAW / 32 * 32 : QMAX;
