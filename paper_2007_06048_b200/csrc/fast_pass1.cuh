@@ -4,10 +4,10 @@
 //        psi_a = b_a * psi_a + a_a * D1_a(p_cur)   over every damping run.
 //
 // k_p1: a persistent, warp-specialised TMA stream.  One work item is a run x a
-// 32 x 16 x-y tile x a z chunk.  The producer lane streams, per plane, the
+// 32 x 16 x-y tile x a z chunk.  Producer lane 0 streams, per plane, the
 // p_cur box the axis' first derivative needs (x halo for x runs, y halo for y
-// runs, a 2R+1-plane ring for z runs) and the psi tile into shared memory;
-// four consumer warps (one float4 of x points per thread) compute the new psi
+// runs, a 2R+1-plane ring for z runs), lane 1 the psi tiles, into shared
+// memory; four consumer warps (one float4 of x points per thread) compute the new psi
 // and store it with coalesced 16-byte global stores.  Bytes in flight are held
 // by TMA, not registers, so the kernel streams at HBM rate.
 #pragma once
