@@ -55,6 +55,8 @@ const Tunable kTunables[] = {
     {"inner_zt", 48},    // k_inner planes per work item (target)
     {"inner_ctas", 0},   // cap on the interior kernel's CTAs beside the CPML kernels (0: every slot)
     {"bnd_zt", 12},      // k_bnd planes per work item (target)
+    {"bnd_whole", -1},   // k_bnd tiles of at most this many planes (the Z slabs) as one item, queued
+                         // first: -1 auto (64 on grids over 30 M points, else 0)
     {"p1_zt", 16},       // k_p1 planes per work item (target)
     {"field_stagger", 1024},  // pressure / c field k starts k x this many floats into its allocation
                             // (240^3: the fast step mode in 6 of 7 engines vs 2-3 of 7 unstaggered)

@@ -161,9 +161,23 @@ struct Item {
     int tag, ty, zlo, zhi;
 };
 void wave_items(const std::vector<Item>& tiles, int ctas, double target,
-                std::vector<int4>& out, bool even = false) {
+                std::vector<int4>& out, bool even = false, int whole_le = 0) {
     out.clear();
     if (tiles.empty()) return;
+    // tiles of at most whole_le planes: one item each, first in the queue
+    // (long items first; no z-window warm-up per chunk for short tiles)
+    if (whole_le > 0) {
+        std::vector<Item> rest;
+        for (const auto& t : tiles)
+            if (t.zhi - t.zlo <= whole_le)
+                out.push_back(make_int4(t.tag, t.ty, t.zlo, t.zhi));
+            else
+                rest.push_back(t);
+        std::vector<int4> more;
+        wave_items(rest, ctas, target, more, even, 0);
+        out.insert(out.end(), more.begin(), more.end());
+        return;
+    }
     long long tp = 0;
     int zmax = 0;
     for (const auto& t : tiles) {
@@ -545,9 +559,9 @@ private:
     }
 
     void finish_work(Work& w, const std::vector<Item>& tiles, int ctas, double target,
-                     bool even = false) {
+                     bool even = false, int whole_le = 0) {
         std::vector<int4> items;
-        wave_items(tiles, ctas, target, items, even);
+        wave_items(tiles, ctas, target, items, even, whole_le);
         w.nitems = (int)items.size();
         w.ctas = std::max(1, std::min(ctas, w.nitems));
         w.segs.set(items, stream_setup_);
@@ -634,7 +648,13 @@ private:
         }
         if (items.empty()) return w;
         w.empty = false;
-        finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_, (tuning("even_chunks") & 2) != 0);
+        // short tiles (the Z slabs) as whole items on big grids: 512^3 729.8 ->
+        // 722.3 us, r=8 1340 -> 1318, 1000^3 3910 -> 3878; at 240^3 (too few items
+        // per CTA to balance 27-plane items) 141.2 -> 141.8, so auto = off there
+        long long bw = tuning("bnd_whole");
+        if (bw < 0) bw = (double)lay_.n[0] * lay_.n[1] * lay_.n[2] > 3.0e7 ? 64 : 0;
+        finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_, (tuning("even_chunks") & 2) != 0,
+                    (int)bw);
         return w;
     }
 
