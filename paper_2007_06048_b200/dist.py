@@ -64,10 +64,11 @@ def validate_cuts(cuts: Sequence[int], n: int, nd: int, radius: int) -> None:
 
 # Relative cost of a plane inside a z damping layer, measured on B200: every
 # rank's slab of 512^3 / 1000^3 timed alone (tools/scaling_projection.py,
-# profiles/r02_scaling_projection.json) gives 2.7-3.2x the time of an
-# undamped plane, against 1.9x in the byte model (the z runs' pass-1 chains
-# and the Z-slab tiles cost more than their bytes).
-ZDAMP_PLANE_WEIGHT = 3.1
+# profiles/r02_scaling_projection.json) gives 2.4-2.8x the time of an
+# undamped plane on the final round-2 kernels (3.1x before the pass-1 stage
+# lane and the boundary work-item changes), against 1.9x in the byte model
+# (the z runs' pass-1 chains and the Z-slab tiles cost more than their bytes).
+ZDAMP_PLANE_WEIGHT = 2.7
 
 
 def plane_costs(n: Sequence[int], nd: Sequence[int], zdamp_weight: float = ZDAMP_PLANE_WEIGHT
