@@ -605,8 +605,9 @@ private:
             for (int ty = 0; ty < tiles_y; ++ty)
                 for (int tx = 0; tx < tiles_x; ++tx) tiles.push_back(Item{tx, ty, r.first, r.second});
         // the target scales with the z-window warm-up (2R planes per item):
-        // k_innerw at r = 8 with 96-plane items 1318 -> 1292 us/step at 512^3
-        finish_work(w, tiles, sms_ * (wk ? 1 : inner_per_sm_), inner_zt_ * std::max(1, R / 4),
+        // k_innerw at r = 8 with 96-plane items 1318 -> 1292 us/step at 512^3,
+        // r = 2 with 24-plane items 676-682 -> 665-669
+        finish_work(w, tiles, sms_ * (wk ? 1 : inner_per_sm_), inner_zt_ * R / 4.0,
                     (tuning("even_chunks") & 1) != 0);
         return w;
     }
