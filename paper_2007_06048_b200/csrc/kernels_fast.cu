@@ -657,8 +657,9 @@ private:
         long long bw = tuning("bnd_whole");
         if (bw < 0) bw = (double)lay_.n[0] * lay_.n[1] * lay_.n[2] > 3.0e7 ? 64 : 0;
         // (the target scales with the z warm-up like the interior's: r = 8 with
-        // 24-plane items 1293 -> 1263 us/step at 512^3, 229 -> 223 at 240^3)
-        finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_ * std::max(1, R / 4),
+        // 24-plane items 1293 -> 1263 us/step at 512^3, 229 -> 223 at 240^3;
+        // r = 2 with 6-plane items 131.0 -> 129.0 at 240^3)
+        finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_ * R / 4.0,
                     (tuning("even_chunks") & 2) != 0, (int)bw);
         return w;
     }
