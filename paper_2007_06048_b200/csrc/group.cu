@@ -106,6 +106,7 @@ struct mm_cd_group {
     int edges[4] = {0, 0, 0, 0};        // plane ranges next to the cuts
     int nedge = 0;
     int ilo = 0, ihi = 0;               // interior plane range
+    bool side = false;                  // this step's interior kernel runs on the side stream
     long long centre = 0;               // device offset of the slab centre (finiteness check)
 
     ~mm_cd_group() {
@@ -165,7 +166,12 @@ struct mm_cd_group {
         mm_cd_engine& E = *e;
         const StepParams sp = E.params();
         const bool fst = E.mode != MM_MODE_STRICT && E.fast;
+        // the interior planes need p_cur only: forked from the step's start,
+        // beside pass 1 (the single-engine step's overlap)
+        side = false;
+        if (fst && ihi > ilo) E.fast->fork_point(E.stream);
         E.pass1();
+        if (fst && ihi > ilo) side = E.fast->interior_side(sp, ilo, ihi);
         // the planes next to the cuts on their own stream, issued first (the
         // persistent interior kernels then fill the SMs they leave), so the
         // transfer waits for them only, not for the interior
@@ -221,10 +227,11 @@ struct mm_cd_group {
         mm_cd_engine& E = *e;
         const StepParams sp = E.params();
         const bool fst = E.mode != MM_MODE_STRICT && E.fast;
-        // the interior planes, concurrent with the transfer
+        // the interior planes' boundary kernel (the interior kernel is already
+        // running on the side stream), concurrent with the transfer
         if (ihi > ilo) {
             if (fst)
-                E.fast->update_overlap(sp, ilo, ihi, E.stream);
+                E.fast->finish_overlap(sp, ilo, ihi, E.stream, side);
             else
                 E.update(0, ilo, ihi);
         }
@@ -319,8 +326,13 @@ int mm_cd_group_create(const mm_grid* global, const int* cuts, int world, int ra
     rc = mm_cd_create(&lg, off, global->n, vp_local, opts, dt, vmax, device, mode, &g->e);
     if (rc) return rc;
     MM_CUDA(cudaSetDevice(device));
-    MM_CUDA(cudaStreamCreateWithFlags(&g->cs, cudaStreamNonBlocking));
-    MM_CUDA(cudaStreamCreateWithFlags(&g->es, cudaStreamNonBlocking));
+    // the edge planes and the halo transfer gate the neighbours' next step:
+    // their streams at the greatest priority, so their CTAs are dispatched
+    // before the interior and boundary kernels of the same step
+    int prio_lo = 0, prio_hi = 0;
+    MM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    MM_CUDA(cudaStreamCreateWithPriority(&g->cs, cudaStreamNonBlocking, prio_hi));
+    MM_CUDA(cudaStreamCreateWithPriority(&g->es, cudaStreamNonBlocking, prio_hi));
     MM_CUDA(cudaEventCreateWithFlags(&g->ev_p1, cudaEventDisableTiming));
     MM_CUDA(cudaEventCreateWithFlags(&g->ev_edges, cudaEventDisableTiming));
     MM_CUDA(cudaEventCreateWithFlags(&g->ev_comm, cudaEventDisableTiming));

@@ -392,18 +392,26 @@ public:
         launch_boundary(p, zr, s);
     }
 
-    void update_overlap(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) override {
-        const bool fc = fast_cpml(p);
-        if (!fc || zmode_ != 0 || !overlap_) {
-            update(p, 0, z_lo, z_hi, s);
-            return;
-        }
-        MM_CUDA(cudaEventRecord(fork_, s));
+    void fork_point(cudaStream_t s) override {
+        if (overlap_) MM_CUDA(cudaEventRecord(fork_, s));
+    }
+    bool interior_side(const StepParams& p, int z_lo, int z_hi) override {
+        if (!fast_cpml(p) || zmode_ != 0 || !overlap_) return false;
+        // the interior needs p_cur only: from the step's start (fork_point),
+        // at the side stream's low priority
         MM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
         const int ti = timer.begin("inner", side_);
         launch_inner(p, z_lo, z_hi, kInnerOnly, side_);
         timer.end(ti, side_);
         MM_CUDA(cudaEventRecord(join_, side_));
+        return true;
+    }
+    void finish_overlap(const StepParams& p, int z_lo, int z_hi, cudaStream_t s,
+                        bool side) override {
+        if (!side) {
+            update(p, 0, z_lo, z_hi, s);
+            return;
+        }
         const int tb = timer.begin("boundary", s);
         launch_boundary(p, z_lo, z_hi, s);
         timer.end(tb, s);

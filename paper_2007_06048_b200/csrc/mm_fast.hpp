@@ -22,10 +22,15 @@ public:
     virtual void update(const StepParams& p, int region, int z_lo, int z_hi, cudaStream_t s) = 0;
     // Pass 2 + inner update on the union of n plane ranges [r[2i], r[2i+1]).
     virtual void update_ranges(const StepParams& p, const int* ranges, int n, cudaStream_t s) = 0;
-    // Pass 2 + inner update on planes [z_lo, z_hi), the interior kernel on a
-    // side stream beside the boundary kernel (joined before returning) -- the
-    // z-slab schedule's interior part (group.cu).
-    virtual void update_overlap(const StepParams& p, int z_lo, int z_hi, cudaStream_t s) = 0;
+    // The z-slab schedule's interior part (group.cu), in three calls: the
+    // step's start on s (before pass 1); the interior kernel of planes
+    // [z_lo, z_hi) on the side stream from that point (true) -- or false when
+    // this layout has no side-stream interior; then the boundary kernel of
+    // those planes on s and the join (or, after false, the whole update).
+    virtual void fork_point(cudaStream_t s) = 0;
+    virtual bool interior_side(const StepParams& p, int z_lo, int z_hi) = 0;
+    virtual void finish_overlap(const StepParams& p, int z_lo, int z_hi, cudaStream_t s,
+                                bool side) = 0;
     // One whole step (pass 1, update, source injection); src_off < 0: no source.
     virtual void step(const StepParams& p, long long src_off, float amp, const float* amp_dev,
                       const int* step_dev, cudaStream_t s) = 0;
