@@ -235,6 +235,16 @@ struct mm_cd_engine {
             fast->update_ranges(s, r, n, stream);
         }
     }
+    // The deferred epilogue of the last host-driven step (see full_step):
+    // launched by the next API call on this engine (use() in engine.cu).
+    Epilogue pending_ep;
+    bool ep_pending = false;
+    void flush_epilogue() {
+        if (!ep_pending) return;
+        ep_pending = false;
+        launch_epilogue(pending_ep, stream);
+    }
+
     // One step: the update kernels, then k_epilogue (injection, free surface
     // and -- from mm_cd_run -- the receiver sample and the step counter).
     void full_step(float amp, const int* src, const float* amp_dev, int* step_dev,
@@ -269,7 +279,16 @@ struct mm_cd_engine {
         ep.check_off = check_off;
         ep.done = counters.ptr + 2;
         ep.pdl = fst && tuning("epi_pdl") != 0;
-        launch_epilogue(ep, stream);
+        // a host-driven step's epilogue waits for the next API call: when that
+        // is mm_cd_record (the reference's step-then-record loop) the receiver
+        // sample rides in the epilogue instead of a second launch
+        if (te < 0 && !amp_dev && !step_dev && !rec && check_off < 0 &&
+            tuning("defer_epilogue") != 0) {
+            pending_ep = ep;
+            ep_pending = true;
+        } else {
+            launch_epilogue(ep, stream);
+        }
         if (te >= 0) fast->timer.end(te, stream);
         rotate();
         ++steps;

@@ -60,6 +60,7 @@ const Tunable kTunables[] = {
     {"p1_zt", 16},       // k_p1 planes per work item (target)
     {"field_stagger", 1024},  // pressure / c field k starts k x this many floats into its allocation
                             // (240^3: the fast step mode in 6 of 7 engines vs 2-3 of 7 unstaggered)
+    {"defer_epilogue", 1},  // host-driven steps: epilogue launched by the next call (fuses record)
     {"even_chunks", 5},  // equal-length z chunks per tile (bit mask: 1 interior, 2 boundary, 4 pass-1 x/y;
                          // 240^3: 143.6 with 5, 145.0 with 0, boundary chunks 146.5)
     {"zslabs", -1},      // Z slabs: -1 auto, 0 k_bnd tiles, 1 k_zslab after k_inner, 2 k_zslab columns
@@ -172,9 +173,10 @@ using namespace mmb;
 
 namespace {
 
-void use(mm_cd_engine* e) {
+void use(mm_cd_engine* e, bool flush = true) {
     need(e, "engine");
     MM_CUDA(cudaSetDevice(e->device));
+    if (flush) e->flush_epilogue();  // a host-driven step's deferred epilogue
 }
 
 }  // namespace
@@ -630,10 +632,19 @@ int mm_cd_set_receivers(mm_cd_engine* e, const int* ijk, int nreceivers, int cap
 
 int mm_cd_record(mm_cd_engine* e, int step) {
     MM_API_BEGIN
-    use(e);
+    use(e, false);
     if (step < 0 || step >= e->cap) raise(ST_INVAL, "record step outside the trace capacity");
     RecParams rp{e->p[e->ic].ptr, e->rec_offs.ptr, e->traces.ptr, e->nrec, step, nullptr};
-    launch_record(rp, nullptr, e->stream);
+    if (e->ep_pending && e->pending_ep.p == rp.p) {
+        // right after a host-driven step: the sample rides in its epilogue
+        // (the values it reads are the ones the epilogue leaves: injection and
+        // free surface applied)
+        e->pending_ep.rec = rp;
+        e->flush_epilogue();
+    } else {
+        e->flush_epilogue();
+        launch_record(rp, nullptr, e->stream);
+    }
     MM_API_END
 }
 

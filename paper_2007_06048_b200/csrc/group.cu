@@ -166,6 +166,7 @@ struct mm_cd_group {
         mm_cd_engine& E = *e;
         const StepParams sp = E.params();
         const bool fst = E.mode != MM_MODE_STRICT && E.fast;
+        E.flush_epilogue();  // a host-driven mm_cd_step on this engine before the group's
         // the interior planes need p_cur only: forked from the step's start,
         // beside pass 1 (the single-engine step's overlap)
         side = false;
