@@ -127,7 +127,12 @@ int mm_cd_create(const mm_grid* local, const int offset[3], const int global_n[3
 int mm_cd_destroy(mm_cd_engine* e);
 
 /* ref: propagator.hpp:103-104 step(amp, src).  src_local: 3 ints in local
- * interior coordinates, or NULL when this engine does not own the source. */
+ * interior coordinates, or NULL when this engine does not own the source.
+ * The step's last kernel (source injection, free surface) is launched by the
+ * next call on this engine -- mm_cd_record then samples inside it -- so work
+ * a host enqueues on the engine stream itself must follow a call such as
+ * mm_cd_stream or mm_cd_synchronize (tuning "defer_epilogue" = 0: launched at
+ * once). */
 int mm_cd_step(mm_cd_engine* e, float amp, const int* src_local);
 
 /* Sub-phases of one step, in the reference order (propagator_impl.hpp:
@@ -207,7 +212,8 @@ int mm_cd_kernel_timing(mm_cd_engine* e, int on);
 int mm_cd_kernel_times(mm_cd_engine* e, int cap, char (*names)[32], double* total_ms,
                        long long* launches, int* n);
 
-/* CUDA stream (cudaStream_t) the engine launches on. */
+/* CUDA stream (cudaStream_t) the engine launches on (launches a deferred
+ * step epilogue first, see mm_cd_step). */
 int mm_cd_stream(mm_cd_engine* e, void** stream);
 /* Device pointer + byte size of the r z-planes of p_cur on one side:
  * side 0 = low z, 1 = high z; which 0 = owned edge planes (send),
