@@ -256,7 +256,14 @@ struct mm_cd_group {
         if (a.rec) ep.rec = *a.rec;
         ep.check_off = a.rec && a.rec->bad_step ? centre : -1;
         ep.done = E.counters.ptr + 2;
-        launch_epilogue(ep, E.stream);
+        // a host-driven step's epilogue waits for the next call on the engine,
+        // as in mm_cd_step: a following mm_cd_record samples inside it
+        if (!a.amp_dev && !a.step_dev && !a.rec && tuning("defer_epilogue") != 0) {
+            E.pending_ep = ep;
+            E.ep_pending = true;
+        } else {
+            launch_epilogue(ep, E.stream);
+        }
         E.rotate();
         ++E.steps;
     }
