@@ -322,6 +322,45 @@ def test_step_schedule_variants_bitwise(mm, knobs):
         assert np.array_equal(a, b), f"{int(np.count_nonzero(a != b))} points differ"
 
 
+def test_deferred_epilogue_call_sequences(mm):
+    """A host-driven step's epilogue is launched by the next call (record
+    fuses it): every mix of step / record / pressure / run / synchronize gives
+    the same fields and traces as launching it at once (defer_epilogue=0)."""
+    n, nd, steps = (64, 60, 72), (9, 9, 9), 24
+    grid = mm.make_grid(n, (20.0, 20.0, 20.0))
+    model = mm.random_model(grid, seed=4)
+    opts = mm.EngineOptions(ndamping=nd, taper=True, free_surface=True)
+    w = mm.ricker(25.0, 1.0e-3, steps).samples
+    src = (32, 30, 36)
+    geo = mm.default_receivers(grid, nd)
+
+    def run():
+        e = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp, opts, 1.0e-3, model.vmax)
+        e.set_receivers(geo.receivers, steps)
+        snaps = []
+        for s in range(steps):
+            e.step(float(w[s]), src)
+            if s % 3 == 0:
+                e.record(s)                      # fused into the pending epilogue
+            elif s % 3 == 1:
+                snaps.append(e.pressure())       # flushes, then reads
+                e.record(s)                      # separate record kernel
+            else:
+                e.synchronize()
+                e.record(s)
+        out = (e.pressure(), e.pressure_prev(), e.traces(steps), snaps)
+        del e
+        return out
+
+    with tuned(defer_epilogue=0):
+        want = run()
+    got = run()
+    for a, b in zip(got[:3], want[:3]):
+        assert np.array_equal(a, b)
+    for a, b in zip(got[3], want[3]):
+        assert np.array_equal(a, b)
+
+
 def test_two_engine_zslab_halo_exchange_bitwise(mm):
     """Two z-slab engines on one device, halos moved through the C-ABI plane
     pointers, equal the single engine (test_dist.cpp:107-118 restated)."""
