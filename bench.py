@@ -287,16 +287,11 @@ def run_ours(args):
     kms = {k: v[0] / v[1] for k, v in kt.items() if v[1] > 0}
     klaunch = {k: int(v[1]) for k, v in kt.items()}
     cpml_path = eng.cpml_path()
-    # one engine at a time: a second live engine in the process costs ~8 % per
-    # step (shared hardware queues), so the e2e engine gets the GPU to itself
-    eng.close()
-    del eng
-    torch.cuda.synchronize()
-    # e2e through the public API with host buffers
-    eng2 = mm.AcousticCdEngine(grid, (0, 0, 0), n, model.vp,
-                               mm.EngineOptions(ndamping=nd, taper=True), dt, model.vmax,
-                               device=local, mode=args.mode)
-    eng2.set_receivers(geo.receivers, total)
+    # e2e through the public API with host buffers, on the same engine (the
+    # wavefield just continues): a second engine would add a second set of
+    # streams and allocations, whose placement alone moved a 240^3 step
+    # between 137 and 147 us
+    eng2 = eng
     host_out = torch.empty((args.steps, nrec), dtype=torch.float32, pin_memory=True).numpy()
     for s in range(args.warmup):
         eng2.step(float(w[s]), src)

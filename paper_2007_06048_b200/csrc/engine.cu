@@ -55,6 +55,9 @@ const Tunable kTunables[] = {
     {"inner_zt", 48},    // k_inner planes per work item (target)
     {"inner_ctas", 0},   // cap on the interior kernel's CTAs beside the CPML kernels (0: every slot)
     {"bnd_zt", 12},      // k_bnd planes per work item (target)
+    {"bnd_tail", 15},    // the last % of the boundary queue in half-length items: CTAs that finish
+                         // early take the small ones (240^3: 141-144.5 -> 136.1 us/step; a per-CTA
+                         // globaltimer trace showed k_bnd CTAs ending from 56 to 80+ us)
     {"bnd_whole", -1},   // k_bnd tiles of at most this many planes (the Z slabs) as one item, queued
                          // first: -1 auto (64 on grids over 30 M points, else 0)
     {"p1_zt", 16},       // k_p1 planes per work item (target)

@@ -567,9 +567,27 @@ private:
     }
 
     void finish_work(Work& w, const std::vector<Item>& tiles, int ctas, double target,
-                     bool even = false, int whole_le = 0) {
+                     bool even = false, int whole_le = 0, int tail_pct = 0) {
         std::vector<int4> items;
         wave_items(tiles, ctas, target, items, even, whole_le);
+        // (tuning bnd_tail) the last tail_pct % of the queue in half-length
+        // items: CTAs that finish early take the small ones
+        if (tail_pct > 0) {
+            const size_t keep = items.size() - items.size() * (size_t)tail_pct / 100;
+            std::vector<int4> out(items.begin(), items.begin() + keep);
+            for (size_t i = keep; i < items.size(); ++i) {
+                const int4 t = items[i];
+                const int len = t.w - t.z;
+                if (len >= 8) {
+                    const int mid = t.z + len / 2;
+                    out.push_back(make_int4(t.x, t.y, t.z, mid));
+                    out.push_back(make_int4(t.x, t.y, mid, t.w));
+                } else {
+                    out.push_back(t);
+                }
+            }
+            items.swap(out);
+        }
         w.nitems = (int)items.size();
         w.ctas = std::max(1, std::min(ctas, w.nitems));
         w.segs.set(items, stream_setup_);
@@ -668,7 +686,7 @@ private:
         // 24-plane items 1293 -> 1263 us/step at 512^3, 229 -> 223 at 240^3;
         // r = 2 with 6-plane items 131.0 -> 129.0 at 240^3)
         finish_work(w, items, sms_ * bnd_per_sm_, bnd_zt_ * R / 4.0,
-                    (tuning("even_chunks") & 2) != 0, (int)bw);
+                    (tuning("even_chunks") & 2) != 0, (int)bw, (int)tuning("bnd_tail"));
         return w;
     }
 
