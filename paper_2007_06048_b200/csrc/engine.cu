@@ -58,6 +58,10 @@ const Tunable kTunables[] = {
     {"bnd_tail", 15},    // the last % of the boundary queue in half-length items: CTAs that finish
                          // early take the small ones (240^3: 141-144.5 -> 136.1 us/step; a per-CTA
                          // globaltimer trace showed k_bnd CTAs ending from 56 to 80+ us)
+    {"smem_carveout", -1},   // (experiment) L1 / shared split (percent shared) of every step kernel;
+                             // -1 driver default (100: same step time, pass 1's kernels reordered)
+    {"p1x_ctas", 0},     // (experiment) pass-1 x/y CTAs per SM (0: as many as fit; 2-3 let the z
+                         // and x/y launches start together, but x/y then runs longer: no gain)
     {"bnd_whole", -1},   // k_bnd tiles of at most this many planes (the Z slabs) as one item, queued
                          // first: -1 auto (64 on grids over 30 M points, else 0)
     {"p1_zt", 16},       // k_p1 planes per work item (target)

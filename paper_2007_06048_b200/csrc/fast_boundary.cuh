@@ -187,6 +187,7 @@ template <int R, int ORD>
 __global__ void __maxnreg__(BndCfg<R>::MAXREG)
     k_bnd(const __grid_constant__ BndMaps M, const BndParams P) {
     using C = BndCfg<R>;
+    MM_TRACE_BEGIN
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
     float* qring = ring + C::NS * C::PPLANE;
@@ -590,6 +591,7 @@ __global__ void __maxnreg__(BndCfg<R>::MAXREG)
             if (++rel == C::NS) rel = 0;
         }
     }
+    MM_TRACE_END(3)
 }
 
 }  // namespace fast

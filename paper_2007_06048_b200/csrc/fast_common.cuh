@@ -80,6 +80,31 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
         : "memory");
 }
+// (diagnostics, build with -DMM_TRACE) per-CTA start / end globaltimer
+#ifdef MM_TRACE
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// records (kid, sm, t0, t1) into a device ring read by mm_trace_dump
+__device__ unsigned long long g_mm_trace[4 * 65536];
+__device__ unsigned int g_mm_trace_n;
+#define MM_TRACE_BEGIN const unsigned long long mm_t0 = gtimer();
+#define MM_TRACE_END(kid)                                                              \
+    if (threadIdx.x == 0) {                                                           \
+        unsigned sm;                                                                  \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));                               \
+        const unsigned i = atomicAdd(&g_mm_trace_n, 1u) % 65536u;                      \
+        g_mm_trace[4 * i] = (unsigned long long)(kid);                                \
+        g_mm_trace[4 * i + 1] = sm;                                                   \
+        g_mm_trace[4 * i + 2] = mm_t0;                                                \
+        g_mm_trace[4 * i + 3] = gtimer();                                             \
+    }
+#else
+#define MM_TRACE_BEGIN
+#define MM_TRACE_END(kid)
+#endif
 // Programmatic dependent launch: wait for the preceding grid's memory / let
 // the dependent grid launch.
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, InnerCfg<R>::MINB)
     k_inner(const __grid_constant__ CUtensorMap tm_pc, const __grid_constant__ CUtensorMap tm_pp,
             const __grid_constant__ CUtensorMap tm_cv, const InnerParams P) {
     using C = InnerCfg<R>;
+    MM_TRACE_BEGIN
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
     float* qring = ring + C::QW * C::PLANE;
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(InnerCfg<R>::NT, InnerCfg<R>::MINB)
         qissue = qcons;
     }
     wq_done(P.wq);
+    MM_TRACE_END(2)
 }
 
 // ---------------------------------------------------------------- z columns

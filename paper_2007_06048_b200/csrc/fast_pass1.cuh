@@ -117,6 +117,7 @@ template <int R, int ORD, bool Z>
 __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
     k_p1(const __grid_constant__ P1Maps M, const P1Params P) {
     using C = P1Cfg<R, Z>;
+    MM_TRACE_BEGIN
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
     float* qring = ring + C::NS * C::PSLOT;
@@ -500,6 +501,7 @@ __global__ void __launch_bounds__(P1Cfg<R, Z>::NT)
         }
         }  // if constexpr (Z)
     }
+    MM_TRACE_END(Z ? 0 : 1)
 }
 
 }  // namespace fast

@@ -132,6 +132,22 @@ struct Box {
     int lo[3], hi[3];
 };
 
+// Dynamic shared memory limit of a kernel, and the L1 / shared-memory split
+// the step kernels run with (tuning smem_carveout, experiment: -1 leaves the
+// driver's choice).  Per-CTA globaltimer traces (MM_TRACE builds,
+// mm_trace_dump) show the four persistent kernels of a step running one after
+// another, not side by side: a grid's CTAs are dispatched in order within a
+// priority, and each kernel's resident CTAs leave no room for the next one's;
+// a common carveout only reorders them.
+template <typename F>
+void set_smem(F* fn, int bytes) {
+    MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const long long co = tuning("smem_carveout");
+    if (co >= 0)
+        MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)co));
+}
+
 // Launch with programmatic dependent launch allowed (PDL): the kernel may start
 // while the previous kernel in the stream drains; it orders its dependent
 // reads itself (griddepcontrol.wait).
@@ -303,16 +319,13 @@ public:
         MM_CUDA(cudaGetDeviceProperties(&prop, device));
         sms_ = prop.multiProcessorCount;
         for (auto fn : {k_inner<R, 1>, k_inner<R, 2>})
-            MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)IC::SMEM));
+            set_smem(fn, (int)IC::SMEM);
         if constexpr (kW)
             for (auto fn : {k_innerw<R, 1>, k_innerw<R, 2>})
-                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)IW::SMEM));
+                set_smem(fn, (int)IW::SMEM);
         if constexpr (kCpml) {
             for (auto fn : {k_cpml<RC, 1>, k_cpml<RC, 2>})
-                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)CC::SMEM));
+                set_smem(fn, (int)CC::SMEM);
             int per = 0;
             MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cpml<RC, 2>, CC::NT,
                                                                   CC::SMEM));
@@ -320,29 +333,24 @@ public:
         }
         if constexpr (kZs)
             for (auto fn : {k_zslab<R, 1>, k_zslab<R, 2>})
-                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)ZSlabCfg<R>::SMEM));
+                set_smem(fn, (int)ZSlabCfg<R>::SMEM);
         int per_sm = 0;
         MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inner<R, 2>, IC::NT,
                                                               IC::SMEM));
         inner_per_sm_ = std::max(1, per_sm);
         inner_cap_ = tuning("inner_ctas") > 0 ? (int)tuning("inner_ctas") : 1 << 30;
         if constexpr (kBnd) {
-            MM_CUDA(cudaFuncSetAttribute(k_bnd<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)BC::SMEM));
-            MM_CUDA(cudaFuncSetAttribute(k_bnd<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)BC::SMEM));
+            set_smem(k_bnd<R, 1>, (int)BC::SMEM);
+            set_smem(k_bnd<R, 2>, (int)BC::SMEM);
             MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bnd<R, 2>, BC::NT,
                                                                   BC::SMEM));
             bnd_per_sm_ = std::max(1, per_sm);
         }
         if constexpr (kP1) {
             for (auto fn : {k_p1<R, 1, true>, k_p1<R, 2, true>})
-                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)P1C::SMEM));
+                set_smem(fn, (int)P1C::SMEM);
             for (auto fn : {k_p1<R, 1, false>, k_p1<R, 2, false>})
-                MM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)P1X::SMEM));
+                set_smem(fn, (int)P1X::SMEM);
             MM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p1<R, 2, true>,
                                                                   P1C::NT, P1C::SMEM));
             p1_per_sm_ = std::max(1, per_sm);
@@ -929,7 +937,10 @@ private:
                 std::vector<int4> items;
                 wave_items(tiles, sms_ * p1x_per_sm_, p1_zt_, items, (tuning("even_chunks") & 4) != 0);
                 e.nx = (int)items.size();
-                e.ctas_x = std::max(1, std::min(sms_ * p1x_per_sm_, e.nx));
+                // (tuning p1x_ctas: x/y CTAs per SM; 0 = as many as fit)
+                const long long pxs = tuning("p1x_ctas");
+                const int xper = pxs > 0 ? (int)std::min<long long>(pxs, p1x_per_sm_) : p1x_per_sm_;
+                e.ctas_x = std::max(1, std::min(sms_ * xper, e.nx));
                 e.nz = (int)zitems.size();
                 e.ctas_z = std::max(1, std::min(sms_ * p1_per_sm_, e.nz));
                 items.insert(items.end(), zitems.begin(), zitems.end());
@@ -1274,3 +1285,21 @@ std::unique_ptr<FastPlan> make_fast_plan(const Layout& lay, int device, float* c
 }
 
 }  // namespace mmb
+
+#ifdef MM_TRACE
+// (diagnostics) the per-CTA trace ring of the fast kernels: n records of
+// (kernel id, SM, start ns, end ns); the ring restarts after the read
+extern "C" int mm_trace_dump(unsigned long long* out, int cap, int* n) {
+    unsigned int cnt = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&cnt, mmb::fast::g_mm_trace_n, sizeof cnt);
+    const int m = (int)(cnt < 65536u ? cnt : 65536u);
+    const int k = m < cap ? m : cap;
+    if (k > 0)
+        cudaMemcpyFromSymbol(out, mmb::fast::g_mm_trace, sizeof(unsigned long long) * 4 * (size_t)k);
+    *n = k;
+    const unsigned int zero = 0;
+    cudaMemcpyToSymbol(mmb::fast::g_mm_trace_n, &zero, sizeof zero);
+    return 0;
+}
+#endif
